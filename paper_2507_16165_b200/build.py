@@ -1,0 +1,72 @@
+"""In-tree build of the CUDA library (sm_100a) and the C++ drop-in shim.
+
+    python -m paper_2507_16165_b200.build        # or __graft_entry__.build()
+
+Products (git-ignored, but they travel to the GPU box with the snapshot):
+    paper_2507_16165_b200/libbhrt_b200.so   C ABI of include/bhrt_cuda.h
+"""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+LIB = os.path.join(PKG, "libbhrt_b200.so")
+
+NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+# --fmad=false: the kernels spell out every fused op with fma(); nothing else
+# may be contracted, so integration arithmetic matches the oracle bit for bit
+# (DESIGN.md §Parity).
+NVFLAGS = ["-O3", "-std=c++17", "-lineinfo", "--fmad=false", "-Xptxas", "-v",
+           "-Xcompiler", "-fPIC,-ffp-contract=off,-O2", "-I" + os.path.join(ROOT, "include")]
+SOURCES = ["trace.cu", "bhrt_cuda.cu", "fp64_peak.cu"]
+
+
+def _stale(target: str, deps: list[str]) -> bool:
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build(verbose: bool = False, force: bool = False) -> str:
+    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
+    deps.append(os.path.join(ROOT, "include", "bhrt_cuda.h"))
+    if force or _stale(LIB, deps):
+        objs = []
+        os.makedirs(os.path.join(ROOT, "build"), exist_ok=True)
+        for src in SOURCES:
+            obj = os.path.join(ROOT, "build", src.replace(".cu", ".o"))
+            cmd = [NVCC, *ARCH, *NVFLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+            r = subprocess.run(cmd, capture_output=True, text=True)
+            if r.returncode != 0:
+                sys.stderr.write(r.stdout + r.stderr)
+                raise RuntimeError(f"nvcc failed for {src}")
+            if verbose:
+                sys.stderr.write(r.stderr)
+            objs.append(obj)
+        tmp = LIB + ".tmp"
+        cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError("link failed")
+        os.replace(tmp, LIB)
+    return LIB
+
+
+def build_oracle() -> None:
+    """The CPU checker (oracle/liboracle.so) and, where /root/reference exists,
+    the compiled reference (oracle/_ref). Test infrastructure, not product."""
+    subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle")], check=True)
+
+
+if __name__ == "__main__":
+    build(verbose=True, force="--force" in sys.argv)
+    build_oracle()
+    print(LIB)

@@ -1,0 +1,561 @@
+// bhrt_cuda.cu — host side of the C ABI (include/bhrt_cuda.h).
+//
+// Owns device state (bhrt_ctx), validates scenes with the reference's rules
+// and error taxonomy (render.cpp:11-20,68-75; geodesic.cpp:19-27;
+// camera.cpp:30-43), hoists the per-frame camera math the reference redoes
+// per ray, and launches the kernels in trace.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <vector>
+
+#include "bhrt_kernel_params.h"
+
+namespace bhrt_b200 {
+
+int launch_trace(const KParams& p, cudaStream_t st, int* launches);
+
+namespace {
+
+constexpr double kPi = 3.141592653589793;
+
+struct HV3 {
+    double x, y, z;
+};
+HV3 hv(const double* a) { return {a[0], a[1], a[2]}; }
+HV3 hsub(HV3 a, HV3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+double hdot(HV3 a, HV3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+HV3 hcross(HV3 a, HV3 b) { return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x}; }
+double hnorm(HV3 a) { return std::sqrt(hdot(a, a)); }
+HV3 hnormalized(HV3 a) {
+    const double n = hnorm(a);
+    return {a.x / n, a.y / n, a.z / n};
+}
+void hput(double* d, HV3 a) { d[0] = a.x; d[1] = a.y; d[2] = a.z; }
+
+int set_info(bhrt_status_info* info, int code, int px, int py, const char* msg) {
+    if (info) {
+        info->code = code;
+        info->px = px;
+        info->py = py;
+        std::snprintf(info->message, sizeof info->message, "%s", msg);
+    }
+    return code;
+}
+
+int cuda_fail(bhrt_status_info* info, cudaError_t e, const char* where) {
+    char buf[200];
+    std::snprintf(buf, sizeof buf, "%s: %s", where, cudaGetErrorString(e));
+    return set_info(info, BHRT_DEVICE, -1, -1, buf);
+}
+
+#define CK(call)                                              \
+    do {                                                      \
+        const cudaError_t e_ = (call);                        \
+        if (e_ != cudaSuccess) return cuda_fail(info, e_, #call); \
+    } while (0)
+
+// camera.cpp:30-43
+bool camera_basis(const bhrt_scene* s, HV3& f, HV3& r, HV3& u) {
+    const HV3 axis = hsub(hv(s->cam_look_at), hv(s->cam_pos));
+    const double len = hnorm(axis);
+    if (len == 0.0) return false;
+    f = {axis.x / len, axis.y / len, axis.z / len};
+    const HV3 rr = hcross(f, {0.0, 1.0, 0.0});
+    if (hnorm(rr) < 1e-9) return false;
+    r = hnormalized(rr);
+    u = hcross(r, f);
+    return true;
+}
+
+int validate_trace(const bhrt_scene* s, bhrt_status_info* info) {
+    if (!(s->epsilon > 0.0) || !(s->escape_radius > 0.0) || s->max_windings < 1 ||
+        !(s->rel_tol > 0.0) || !(s->abs_tol > 0.0))
+        return set_info(info, BHRT_INVALID_ARGUMENT, -1, -1, "trace config: invalid parameter");
+    if (s->integrator < 0 || s->integrator > BHRT_INTEGRATOR_TABLE ||
+        (s->integrator != BHRT_INTEGRATOR_REFERENCE && !(s->step > 0.0)) ||
+        (s->integrator == BHRT_INTEGRATOR_RKF45 && !(s->max_step > 0.0 && s->max_step < 1.0)) ||
+        (s->integrator == BHRT_INTEGRATOR_REFERENCE && (s->disk_enabled || s->n_spheres > 0)) ||
+        !(s->chord_dphi > 0.0) || (s->n_spheres > 0 && s->spheres == nullptr) ||
+        s->n_spheres < 0 || s->n_spheres > kMaxSpheres ||
+        (s->sky_kind == BHRT_SKY_CHECKER && (s->checker_nu < 1 || s->checker_nv < 1)))
+        return set_info(info, BHRT_INVALID_ARGUMENT, -1, -1, "scene extension: invalid parameter");
+    HV3 f, r, u;
+    if (!camera_basis(s, f, r, u))
+        return set_info(info, BHRT_INVALID_ARGUMENT, -1, -1, "camera: degenerate orientation");
+    return 0;
+}
+
+// RKF45 controller tables: f_q = 0.9 * 2^(-(q+1)/20), clamped.
+void factor_tables(double* grow, double* shrink) {
+    for (int i = 0; i < kQN; ++i) {
+        const int q = kQMin + i;
+        const double f = 0.9 * std::pow(2.0, -static_cast<double>(q + 1) / 20.0);
+        grow[i] = f < 0.2 ? 0.2 : (5.0 < f ? 5.0 : f);
+        shrink[i] = f < 0.1 ? 0.1 : (0.9 < f ? 0.9 : f);
+    }
+}
+
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t cap = 0;  // elements
+    int ensure(size_t n) {
+        if (n <= cap) return 0;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        const cudaError_t e = cudaMalloc(&p, sizeof(T) * std::max<size_t>(n, 1));
+        if (e != cudaSuccess) return -1;
+        cap = n;
+        return 0;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+}  // namespace
+}  // namespace bhrt_b200
+
+using namespace bhrt_b200;
+
+struct bhrt_ctx {
+    int device = 0;
+    bool has_scene = false;
+    KParams kp{};
+    bhrt_scene scene{};
+    DevBuf<uint8_t> sky;
+    DevBuf<bhrt_sphere> spheres;
+    DevBuf<double> tables;
+    DevBuf<bhrt_ray_record> records;
+    DevBuf<uint8_t> out;
+    DevBuf<unsigned long long> stats;
+    DevBuf<unsigned int> queue;
+    cudaStream_t last_stream = nullptr;
+    int launches = 0;
+    int pending = 0;
+    int32_t last_rows = 0;
+    unsigned long long host_stats[4] = {0, 0, 0, 0};
+};
+
+extern "C" {
+
+int32_t bhrt_cuda_abi_version(void) { return BHRT_CUDA_ABI_VERSION; }
+
+void bhrt_scene_defaults(bhrt_scene* s) {
+    std::memset(s, 0, sizeof *s);
+    s->mass = 1.0;
+    s->cam_pos[2] = -20.0;
+    s->vertical_fov = 60.0 * kPi / 180.0;
+    s->width = 256;
+    s->height = 256;
+    s->spp = 1;
+    s->max_windings = 10;
+    s->seed = 1;
+    s->epsilon = 0.05;
+    s->escape_radius = 1e4;
+    s->rel_tol = 1e-10;
+    s->abs_tol = 1e-12;
+    s->integrator = BHRT_INTEGRATOR_REFERENCE;
+    s->sky_kind = BHRT_SKY_IMAGE;
+    s->step = 1e-2;
+    s->max_step = 0.1;
+    s->chord_dphi = 0.01;
+    s->checker_nu = 16;
+    s->checker_nv = 8;
+    const double ca[3] = {0.9, 0.9, 0.9}, cb[3] = {0.1, 0.1, 0.15};
+    const double di[3] = {1.0, 0.95, 0.8}, dout[3] = {0.8, 0.25, 0.05};
+    const double l[3] = {0.5, 1.0, -1.0};
+    std::memcpy(s->checker_color_a, ca, sizeof ca);
+    std::memcpy(s->checker_color_b, cb, sizeof cb);
+    s->disk_r_in = 6.0;
+    s->disk_r_out = 20.0;
+    std::memcpy(s->disk_color_in, di, sizeof di);
+    std::memcpy(s->disk_color_out, dout, sizeof dout);
+    std::memcpy(s->light_dir, l, sizeof l);
+    s->ambient = 0.1;
+    s->table_entries = 100000;
+    s->table_samples = 2048;
+    s->table_b_max = 50.0;
+    s->table_dpsi = 0.01;
+}
+
+int bhrt_validate_scene(const bhrt_scene* s, bhrt_status_info* info) {  // render.cpp:11-20
+    set_info(info, 0, -1, -1, "");
+    if (!s) return set_info(info, BHRT_INVALID_ARGUMENT, -1, -1, "scene is NULL");
+    if (s->sky_kind == BHRT_SKY_IMAGE && (s->sky_rgb == nullptr || s->sky_width < 1 || s->sky_height < 1))
+        return set_info(info, BHRT_USAGE, -1, -1, "scene: background image is required");
+    if (s->width < 1 || s->height < 1)
+        return set_info(info, BHRT_USAGE, -1, -1, "scene: image dimensions must be >= 1");
+    if (s->spp < 1) return set_info(info, BHRT_USAGE, -1, -1, "scene: spp must be >= 1");
+    if (s->mass < 0.0) return set_info(info, BHRT_USAGE, -1, -1, "scene: mass must be >= 0");
+    const double d = hnorm(hsub(hv(s->cam_pos), hv(s->center)));
+    if (d <= 2.0 * s->mass)
+        return set_info(info, BHRT_USAGE, -1, -1, "scene: camera must be outside the event horizon");
+    return 0;
+}
+
+int bhrt_make_spheres(uint64_t seed, int32_t n, const double center[3], double shell_min,
+                      double shell_max, double radius_min, double radius_max, bhrt_sphere* out) {
+    if (n < 0 || !(shell_min >= 0.0) || !(shell_max >= shell_min) || !(radius_min > 0.0) ||
+        !(radius_max >= radius_min))
+        return BHRT_INVALID_ARGUMENT;
+    uint64_t x = seed;
+    const auto next = [&x]() {
+        uint64_t z = (x += 0x9e3779b97f4a7c15ULL);
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+        return z ^ (z >> 31);
+    };
+    const auto unit = [&]() { return static_cast<double>(next() >> 11) * 0x1.0p-53; };
+    const double lo3 = shell_min * shell_min * shell_min;
+    const double hi3 = shell_max * shell_max * shell_max;
+    for (int i = 0; i < n; ++i) {
+        const double cz = 2.0 * unit() - 1.0;
+        const double th = 2.0 * kPi * unit();
+        const double rr = std::cbrt(lo3 + unit() * (hi3 - lo3));
+        const double sxy = std::sqrt(1.0 - cz * cz);
+        out[i].center[0] = center[0] + rr * (sxy * std::cos(th));
+        out[i].center[1] = center[1] + rr * cz;
+        out[i].center[2] = center[2] + rr * (sxy * std::sin(th));
+        out[i].radius = radius_min + unit() * (radius_max - radius_min);
+        out[i].albedo[0] = unit();
+        out[i].albedo[1] = unit();
+        out[i].albedo[2] = unit();
+    }
+    return 0;
+}
+
+int bhrt_make_bands(int32_t height, int32_t workers, int32_t* rs, int32_t* re, int32_t cap,
+                    int32_t* count) {  // render.cpp:51-66
+    if (height < 1 || workers < 1) return BHRT_INVALID_ARGUMENT;
+    const int n = std::min(height, workers);
+    if (cap < n) return BHRT_INVALID_ARGUMENT;
+    const int base = height / n, extra = height % n;
+    int row = 0;
+    for (int i = 0; i < n; ++i) {
+        const int rows = base + (i < extra ? 1 : 0);
+        rs[i] = row;
+        re[i] = row + rows;
+        row += rows;
+    }
+    *count = n;
+    return 0;
+}
+
+int32_t bhrt_tile_row_count(int32_t row_start, int32_t row_end, int32_t tile_rows,
+                            int32_t tile_stride, int32_t tile_offset) {
+    if (tile_rows < 1 || tile_stride < 1 || tile_offset < 0 || tile_offset >= tile_stride ||
+        row_end < row_start)
+        return -1;
+    const int rows = row_end - row_start;
+    const int full_tiles = rows / tile_rows, rem = rows % tile_rows;
+    const int ntiles = full_tiles + (rem ? 1 : 0);
+    int count = 0;
+    for (int t = tile_offset; t < ntiles; t += tile_stride) count += (t < full_tiles) ? tile_rows : rem;
+    return count;
+}
+
+double bhrt_flops_per_step(int32_t integrator) {
+    // Algorithmic FP64 flops per accepted step, fma = 2.
+    switch (integrator) {
+        case BHRT_INTEGRATOR_REFERENCE: return 152.0;  // 110 stages + 38 error + 4 controller
+        case BHRT_INTEGRATOR_RK4: return 44.0;         // tests/oracles.hpp:23-30 op count
+        case BHRT_INTEGRATOR_RKF45: return 148.0;      // DESIGN.md §Roofline op count
+        default: return 0.0;
+    }
+}
+
+int bhrt_ctx_create(int32_t device, bhrt_ctx** out, bhrt_status_info* info) {
+    set_info(info, 0, -1, -1, "");
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev)
+        return set_info(info, BHRT_INVALID_ARGUMENT, -1, -1, "bhrt_ctx_create: bad device");
+    CK(cudaSetDevice(device));
+    std::unique_ptr<bhrt_ctx> c(new bhrt_ctx());
+    c->device = device;
+    if (c->stats.ensure(4) || c->queue.ensure(1) || c->tables.ensure(2 * kQN))
+        return set_info(info, BHRT_DEVICE, -1, -1, "bhrt_ctx_create: cudaMalloc failed");
+    double tb[2 * kQN];
+    factor_tables(tb, tb + kQN);
+    CK(cudaMemcpy(c->tables.p, tb, sizeof tb, cudaMemcpyHostToDevice));
+    *out = c.release();
+    return 0;
+}
+
+void bhrt_ctx_destroy(bhrt_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaDeviceSynchronize();
+    c->sky.release();
+    c->spheres.release();
+    c->tables.release();
+    c->records.release();
+    c->out.release();
+    c->stats.release();
+    c->queue.release();
+    delete c;
+}
+
+int bhrt_ctx_set_scene(bhrt_ctx* c, const bhrt_scene* s, bhrt_status_info* info) {
+    int rc = bhrt_validate_scene(s, info);
+    if (rc) return rc;
+    rc = validate_trace(s, info);
+    if (rc) return rc;
+    if (s->integrator == BHRT_INTEGRATOR_TABLE)
+        return set_info(info, BHRT_INVALID_ARGUMENT, -1, -1, "table integrator not built in this version");
+    CK(cudaSetDevice(c->device));
+    CK(cudaDeviceSynchronize());
+    KParams& k = c->kp;
+    std::memset(&k, 0, sizeof k);
+    k.mass = s->mass;
+    k.M3 = 3.0 * s->mass;
+    std::memcpy(k.center, s->center, sizeof k.center);
+    k.u_cap = s->mass > 0.0 ? 1.0 / (2.0 * s->mass) : INFINITY;
+    k.u_esc = 1.0 / s->escape_radius;
+    k.escape_radius = s->escape_radius;
+    k.phi_max = 2.0 * kPi * s->max_windings;
+    k.max_windings = s->max_windings;
+    k.integrator = s->integrator;
+    std::memcpy(k.cam_pos, s->cam_pos, sizeof k.cam_pos);
+    HV3 f, r, u;
+    camera_basis(s, f, r, u);
+    hput(k.forward, f);
+    hput(k.right, r);
+    hput(k.up, u);
+    k.tan_half_y = std::tan(s->vertical_fov / 2.0);  // camera.cpp:46-48
+    const double aspect = static_cast<double>(s->width) / s->height;
+    k.tan_half_x = k.tan_half_y * aspect;
+    k.width = s->width;
+    k.height = s->height;
+    k.spp = s->spp;
+    k.seed = s->seed;
+    k.epsilon = s->epsilon;
+    k.rel_tol = s->rel_tol;
+    k.abs_tol = s->abs_tol;
+    k.step = s->step;
+    k.max_step = s->max_step;
+    k.chord_dphi = s->chord_dphi;
+    k.sky_kind = s->sky_kind;
+    k.checker_nu = s->checker_nu;
+    k.checker_nv = s->checker_nv;
+    std::memcpy(k.checker_a, s->checker_color_a, sizeof k.checker_a);
+    std::memcpy(k.checker_b, s->checker_color_b, sizeof k.checker_b);
+    k.disk_enabled = s->disk_enabled;
+    k.disk_r_in = s->disk_r_in;
+    k.disk_r_out = s->disk_r_out;
+    std::memcpy(k.disk_c_in, s->disk_color_in, sizeof k.disk_c_in);
+    std::memcpy(k.disk_c_out, s->disk_color_out, sizeof k.disk_c_out);
+    k.n_spheres = s->n_spheres;
+    hput(k.light, hnormalized(hv(s->light_dir)));
+    k.ambient = s->ambient;
+    if (s->sky_kind == BHRT_SKY_IMAGE) {
+        const size_t bytes = 3ull * s->sky_width * s->sky_height;
+        if (c->sky.ensure(bytes)) return set_info(info, BHRT_DEVICE, -1, -1, "sky alloc failed");
+        CK(cudaMemcpy(c->sky.p, s->sky_rgb, bytes, cudaMemcpyHostToDevice));
+        k.sky = c->sky.p;
+        k.sky_w = s->sky_width;
+        k.sky_h = s->sky_height;
+    }
+    if (s->n_spheres > 0) {
+        if (c->spheres.ensure(s->n_spheres)) return set_info(info, BHRT_DEVICE, -1, -1, "sphere alloc failed");
+        CK(cudaMemcpy(c->spheres.p, s->spheres, sizeof(bhrt_sphere) * s->n_spheres, cudaMemcpyHostToDevice));
+        k.spheres = c->spheres.p;
+    }
+    k.grow = c->tables.p;
+    k.shrink = c->tables.p + kQN;
+    c->scene = *s;
+    c->has_scene = true;
+    return 0;
+}
+
+int bhrt_ctx_render_async(bhrt_ctx* c, int32_t row_start, int32_t row_end, int32_t tile_rows,
+                          int32_t tile_stride, int32_t tile_offset, uint8_t* d_out,
+                          bhrt_ray_record* d_records, void* stream, bhrt_status_info* info) {
+    set_info(info, 0, -1, -1, "");
+    if (!c || !c->has_scene) return set_info(info, BHRT_INVALID_ARGUMENT, -1, -1, "context has no scene");
+    if (row_start < 0 || row_end > c->scene.height || row_start > row_end)
+        return set_info(info, BHRT_INVALID_ARGUMENT, -1, -1, "render: row range out of bounds");
+    const int32_t rows = bhrt_tile_row_count(row_start, row_end, tile_rows, tile_stride, tile_offset);
+    if (rows < 0) return set_info(info, BHRT_INVALID_ARGUMENT, -1, -1, "render: bad tiling");
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    KParams k = c->kp;
+    k.row_start = row_start;
+    k.row_end = row_end;
+    k.tile_rows = tile_rows;
+    k.tile_stride = tile_stride;
+    k.tile_offset = tile_offset;
+    k.n_rows = rows;
+    const size_t nrec = static_cast<size_t>(rows) * k.width * k.spp;
+    if (!d_records) {
+        if (c->records.ensure(nrec)) return set_info(info, BHRT_DEVICE, -1, -1, "records alloc failed");
+        d_records = c->records.p;
+    }
+    k.records = d_records;
+    k.out = d_out;
+    k.stats = c->stats.p;
+    k.queue = c->queue.p;
+    const unsigned long long init[4] = {0ull, 0ull, 0ull, ULLONG_MAX};
+    CK(cudaMemcpyAsync(c->stats.p, init, sizeof init, cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(c->queue.p, 0, sizeof(unsigned int), st));
+    c->launches = 0;
+    if (rows > 0 && launch_trace(k, st, &c->launches) != 0)
+        return set_info(info, BHRT_INVALID_ARGUMENT, -1, -1, "render: unsupported integrator");
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(c->host_stats, c->stats.p, sizeof c->host_stats, cudaMemcpyDeviceToHost, st));
+    c->last_stream = st;
+    c->pending = 1;
+    c->last_rows = rows;
+    c->kp.row_start = row_start;  // remembered for failure mapping
+    c->kp.row_end = row_end;
+    c->kp.tile_rows = tile_rows;
+    c->kp.tile_stride = tile_stride;
+    c->kp.tile_offset = tile_offset;
+    c->kp.n_rows = rows;
+    return 0;
+}
+
+int bhrt_ctx_finish(bhrt_ctx* c, bhrt_status_info* info) {
+    set_info(info, 0, -1, -1, "");
+    if (!c) return set_info(info, BHRT_INVALID_ARGUMENT, -1, -1, "NULL context");
+    CK(cudaSetDevice(c->device));
+    if (!c->pending) return 0;
+    CK(cudaStreamSynchronize(c->last_stream));
+    c->pending = 0;
+    const unsigned long long fail = c->host_stats[3];
+    if (fail != ULLONG_MAX) {
+        const int j = static_cast<int>(fail / c->kp.width);
+        const int px = static_cast<int>(fail % c->kp.width);
+        const int py = packed_row_to_y(c->kp, j);
+        char msg[96];
+        std::snprintf(msg, sizeof msg, "pixel (%d, %d): numerical failure", px, py);
+        return set_info(info, BHRT_NUMERICAL, px, py, msg);
+    }
+    return 0;
+}
+
+int bhrt_ctx_stats(bhrt_ctx* c, uint64_t* steps, uint64_t* rejected, uint64_t* rays, int32_t* launches) {
+    if (!c) return BHRT_INVALID_ARGUMENT;
+    if (steps) *steps = c->host_stats[0];
+    if (rejected) *rejected = c->host_stats[1];
+    if (rays) *rays = c->host_stats[2];
+    if (launches) *launches = c->launches;
+    return 0;
+}
+
+}  // extern "C"
+
+namespace {
+std::mutex g_ctx_mu;
+std::map<int, bhrt_ctx*> g_ctx;  // one cached context per device for the one-shot API
+
+int cached_ctx(int dev, bhrt_ctx** out, bhrt_status_info* info) {
+    auto it = g_ctx.find(dev);
+    if (it != g_ctx.end()) {
+        *out = it->second;
+        return 0;
+    }
+    const int rc = bhrt_ctx_create(dev, out, info);
+    if (rc == 0) g_ctx[dev] = *out;
+    return rc;
+}
+}  // namespace
+
+extern "C" int bhrt_cuda_render_rows(const bhrt_scene* s, int32_t row_start, int32_t row_end,
+                                     const int32_t* devices, int32_t ndev, uint8_t* out,
+                                     size_t out_len, bhrt_ray_record* records,
+                                     bhrt_status_info* info) {
+    // render.cpp:68-75 validation order: scene, then arguments.
+    int rc = bhrt_validate_scene(s, info);
+    if (rc) return rc;
+    if (row_start < 0 || row_end > s->height || row_start > row_end)
+        return set_info(info, BHRT_INVALID_ARGUMENT, -1, -1, "render: row range out of bounds");
+    const size_t need = 3ull * static_cast<size_t>(row_end - row_start) * s->width;
+    if (out_len < need || (need > 0 && out == nullptr))
+        return set_info(info, BHRT_INVALID_ARGUMENT, -1, -1, "render: output buffer too small");
+    if (row_end == row_start) return 0;
+    rc = validate_trace(s, info);
+    if (rc) return rc;
+
+    std::lock_guard<std::mutex> lock(g_ctx_mu);
+    std::vector<int> devs;
+    if (!devices || ndev <= 0) {
+        int d = 0;
+        CK(cudaGetDevice(&d));
+        devs.push_back(d);
+    } else {
+        devs.assign(devices, devices + ndev);
+    }
+    const int G = static_cast<int>(devs.size());
+    const int tile_rows = 1;  // cyclic rows (7.78x vs 6.35x for bands)
+    std::vector<bhrt_ctx*> ctxs(G);
+    std::vector<int32_t> nrows(G);
+    for (int g = 0; g < G; ++g) {
+        rc = cached_ctx(devs[g], &ctxs[g], info);
+        if (rc) return rc;
+        rc = bhrt_ctx_set_scene(ctxs[g], s, info);
+        if (rc) return rc;
+        nrows[g] = bhrt_tile_row_count(row_start, row_end, tile_rows, G, g);
+        if (ctxs[g]->out.ensure(3ull * nrows[g] * s->width + 1))
+            return set_info(info, BHRT_DEVICE, -1, -1, "output alloc failed");
+        rc = bhrt_ctx_render_async(ctxs[g], row_start, row_end, tile_rows, G, g, ctxs[g]->out.p,
+                                   nullptr, nullptr, info);
+        if (rc) return rc;
+    }
+    int first_fail = 0;
+    long long fail_key = LLONG_MAX;
+    bhrt_status_info tmp;
+    for (int g = 0; g < G; ++g) {
+        const int r = bhrt_ctx_finish(ctxs[g], &tmp);
+        if (r == BHRT_NUMERICAL) {
+            const long long key = static_cast<long long>(tmp.py) * s->width + tmp.px;
+            if (key < fail_key) {
+                fail_key = key;
+                if (info) *info = tmp;
+                first_fail = r;
+            }
+        } else if (r) {
+            if (info) *info = tmp;
+            return r;
+        }
+    }
+    if (first_fail) return first_fail;
+    const size_t row_bytes = 3ull * s->width;
+    for (int g = 0; g < G; ++g) {
+        CK(cudaSetDevice(devs[g]));
+        if (G == 1) {
+            CK(cudaMemcpy(out, ctxs[g]->out.p, row_bytes * nrows[g], cudaMemcpyDeviceToHost));
+        } else {
+            std::vector<uint8_t> stage(row_bytes * nrows[g]);
+            CK(cudaMemcpy(stage.data(), ctxs[g]->out.p, stage.size(), cudaMemcpyDeviceToHost));
+            for (int j = 0; j < nrows[g]; ++j) {
+                const int y = packed_row_to_y(ctxs[g]->kp, j);
+                std::memcpy(out + row_bytes * (y - row_start), stage.data() + row_bytes * j, row_bytes);
+            }
+        }
+        if (records) {
+            const size_t per_row = static_cast<size_t>(s->width) * s->spp;
+            std::vector<bhrt_ray_record> stage(per_row * nrows[g]);
+            CK(cudaMemcpy(stage.data(), ctxs[g]->records.p, sizeof(bhrt_ray_record) * stage.size(),
+                          cudaMemcpyDeviceToHost));
+            for (int j = 0; j < nrows[g]; ++j) {
+                const int y = packed_row_to_y(ctxs[g]->kp, j);
+                std::memcpy(records + per_row * (y - row_start), stage.data() + per_row * j,
+                            sizeof(bhrt_ray_record) * per_row);
+            }
+        }
+    }
+    return 0;
+}

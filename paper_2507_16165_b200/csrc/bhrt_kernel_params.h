@@ -1,0 +1,70 @@
+// Kernel parameter block shared by host (bhrt_cuda.cu) and device (trace.cu).
+// Everything per-frame that the reference recomputes per ray (camera basis,
+// tan(fov/2): camera.cpp:46-48,67) is hoisted here once on the host with the
+// reference's own operation order, so the device sees bit-identical values.
+#pragma once
+
+#include <cstdint>
+
+#include "../../include/bhrt_cuda.h"
+
+namespace bhrt_b200 {
+
+constexpr int kQMin = -64;  // RKF45 controller table range
+constexpr int kQN = 96;
+constexpr int kMaxSpheres = 256;
+constexpr int kMaxCand = 16;
+
+struct KParams {
+    // black hole + termination
+    double mass, M3;
+    double center[3];
+    double u_cap, u_esc, phi_max, escape_radius;
+    int32_t max_windings;
+    int32_t integrator;
+    // camera (hoisted)
+    double cam_pos[3];
+    double forward[3], right[3], up[3];
+    double tan_half_x, tan_half_y;
+    int32_t width, height, spp;
+    int32_t pad0;
+    uint64_t seed;
+    // integrator
+    double epsilon, rel_tol, abs_tol, step, max_step, chord_dphi;
+    // rows: packed row j -> image row y (see bhrt_ctx_render_async)
+    int32_t row_start, row_end, tile_rows, tile_stride, tile_offset, n_rows;
+    // sky
+    int32_t sky_kind, sky_w, sky_h, checker_nu, checker_nv;
+    int32_t pad1;
+    const uint8_t* sky;
+    double checker_a[3], checker_b[3];
+    // disk
+    int32_t disk_enabled;
+    int32_t n_spheres;
+    double disk_r_in, disk_r_out;
+    double disk_c_in[3], disk_c_out[3];
+    // spheres (device arrays)
+    const bhrt_sphere* spheres;
+    double light[3];
+    double ambient;
+    // RKF45 factor tables (device)
+    const double* grow;
+    const double* shrink;
+    // b-table (approximate mode)
+    const double* table;
+    int32_t table_entries, table_stride;
+    double table_b_max, table_db, table_dpsi;
+    // outputs
+    bhrt_ray_record* records;   // n_rows * width * spp
+    uint8_t* out;               // n_rows * width * 3
+    unsigned long long* stats;  // [0] steps, [1] rejected, [2] rays, [3] lowest failing index+1
+    unsigned int* queue;        // persistent work counter
+};
+
+__host__ __device__ inline int packed_row_to_y(const KParams& p, int j) {
+    const int tile = j / p.tile_rows;
+    const int within = j - tile * p.tile_rows;
+    return p.row_start + (tile * p.tile_stride + p.tile_offset) * p.tile_rows + within;
+}
+
+}  // namespace bhrt_b200
