@@ -1,0 +1,346 @@
+#!/usr/bin/env python
+"""Benchmark of the Schwarzschild ray-tracing hot path (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
+
+A step = one full frame of BASELINE.json configs[C] (default C=2: 3840x2160,
+4 jittered spp, disk + 64 spheres, RKF45 tol 1e-9) rendered by all ranks
+(cyclic row tiles) and gathered to rank 0 over NCCL. Prints ONE JSON line on
+rank 0. Metric: Mrays/s (rays = pixels x spp), whole job.
+
+--impl reference times the CPU implementation of the same workload on the
+host cores (rank 0 only): the oracle port of the full scene (the reference
+itself cannot render disk/spheres/RKF45 — SPEC.md:14,171), kind "port".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    0: "config0: 256x256x1spp disk+checker, RK4 dphi=1e-3",
+    1: "config1: 1920x1080x1spp disk+checker, RKF45 tol 1e-9",
+    2: "config2: 3840x2160x4spp jittered, disk r6-30 + 64 Lambertian spheres, RKF45 tol 1e-9",
+}
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        mhz, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                m = float(f[1])
+                mx = float(f[2])
+            except ValueError:
+                continue
+            mhz.append(m)
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        loaded = [m for m in mhz if m > 500] or mhz
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(mhz)}
+
+
+# ---------------------------------------------------------------- CPU legs
+def cpu_port_rows(scene, rows_sel, threads):
+    """Render the selected rows with the oracle's pthread row queue."""
+    import ctypes as C
+    import numpy as np
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_lib import oracle
+    from paper_2507_16165_b200.abi import StatusInfo
+    L = oracle()
+    # contiguous block of rows keeps the oracle's dynamic row queue busy
+    r0, r1 = rows_sel
+    out = np.zeros((r1 - r0) * scene.s.width * 3, np.uint8)
+    info = StatusInfo()
+    t0 = time.perf_counter()
+    rc = L.orc_render_rows(C.byref(scene.s), r0, r1, threads,
+                           out.ctypes.data_as(C.POINTER(C.c_uint8)), None, C.byref(info))
+    dt = time.perf_counter() - t0
+    if rc:
+        raise RuntimeError(f"oracle failed: {info.message}")
+    return (r1 - r0) * scene.s.width * scene.s.spp, dt
+
+
+def centre_band(height: int, rows: int):
+    r0 = max(0, height // 2 - rows // 2)
+    return r0, min(height, r0 + rows)
+
+
+def reference_sky_only(scene, rows: int, threads: int):
+    """The compiled reference (oracle/_ref) on the sky-only projection of the
+    workload (its own render_rows)."""
+    import ctypes as C
+    import numpy as np
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_lib import have_ref, ref
+    from paper_2507_16165_b200 import scenes
+    from paper_2507_16165_b200.abi import StatusInfo
+    if not have_ref():
+        return None
+    proj = scenes.sky_only_projection(scene)
+    r0, r1 = centre_band(proj.s.height, rows)
+    out = np.zeros((r1 - r0) * proj.s.width * 3, np.uint8)
+    info = StatusInfo()
+    t0 = time.perf_counter()
+    rc = ref().ref_render_rows(C.byref(proj.s), r0, r1, threads,
+                               out.ctypes.data_as(C.POINTER(C.c_uint8)), C.byref(info))
+    dt = time.perf_counter() - t0
+    if rc:
+        return None
+    rays = (r1 - r0) * proj.s.width * proj.s.spp
+    return {"value": rays / dt / 1e6, "unit": "Mrays/s", "cores": threads, "kind": "reference",
+            "sample": f"oracle/_ref render_rows (the reference's own code), sky-only projection "
+                      f"of the workload (DOPRI5 eps=0.05 windows, checker baked into a 2048x1024 "
+                      f"PPM), rows [{r0},{r1}) = {rays} rays, {dt:.1f} s"}
+
+
+# ---------------------------------------------------------------- arms
+def run_reference_arm(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return 0
+    from paper_2507_16165_b200 import scenes
+    scene = scenes.config(args.config)
+    threads = os.cpu_count() or 1
+    rows = args.ref_rows
+    band = centre_band(scene.s.height, rows)
+    for _ in range(args.warmup):
+        cpu_port_rows(scene, (band[0], band[0] + 1), threads)
+    tot_rays, tot_s = 0, 0.0
+    per = []
+    for _ in range(args.steps):
+        rays, dt = cpu_port_rows(scene, band, threads)
+        tot_rays += rays
+        tot_s += dt
+        per.append(dt)
+    value = tot_rays / tot_s / 1e6
+    sample = (f"oracle port (C, pthreads) of the full workload, centre rows [{band[0]},{band[1]}) "
+              f"= {tot_rays // args.steps} rays per step")
+    line = {
+        "impl": "reference", "metric": "Mrays/s", "value": value, "unit": "Mrays/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot_s / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOADS[args.config], "width": scene.s.width,
+                   "height": scene.s.height, "spp": scene.s.spp, "parallelism": f"cpu x{threads}"},
+        "cpu_baseline": {"value": value, "unit": "Mrays/s", "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "Mrays/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2507_16165_b200 import native, roofline, scenes
+    from paper_2507_16165_b200.abi import Scene, Sphere
+    from paper_2507_16165_b200.parallel import FrameRenderer
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    scene = scenes.config(args.config)
+    W, H, spp = scene.s.width, scene.s.height, scene.s.spp
+    total_rays = W * H * spp
+
+    fr = FrameRenderer(rank, world, local)
+    fr.set_scene(scene)
+    fr.ctx.set_timing(True)
+    st = torch.cuda.current_stream()
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def step():
+        return fr.render_device(st)
+
+    for _ in range(args.warmup):
+        step()
+        fr.finish()
+    torch.cuda.synchronize()
+    barrier()
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    ms, trace_ms, shade_ms, flops = [], [], [], []
+    stats = None
+    for _ in range(args.steps):
+        flush.zero_()  # L2 flush (256 MiB > 126 MB L2) outside the timed window
+        torch.cuda.synchronize()
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        step()
+        e1.record(st)
+        fr.finish()
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+        t_ms, s_ms = fr.ctx.kernel_ms()
+        trace_ms.append(t_ms)
+        shade_ms.append(s_ms)
+        stats = fr.ctx.stats()
+        flops.append(roofline.launch_flops(scene, stats))
+    clocks = sampler.stop()
+    step_ms = sum(ms) / len(ms)
+    t = torch.tensor([step_ms], device="cuda", dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    step_ms_max = float(t.item())
+    value = total_rays / (step_ms_max * 1e-3) / 1e6
+
+    # ---- e2e through the public API: H2D scene, render, gather, D2H image
+    e2e_ms = []
+    for i in range(max(2, args.steps) + 1):
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        fr.render(scene)
+        torch.cuda.synchronize()
+        dt = (time.perf_counter() - t0) * 1e3
+        if i > 0:
+            e2e_ms.append(dt)
+    te = torch.tensor([sum(e2e_ms) / len(e2e_ms)], device="cuda", dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = total_rays / (float(te.item()) * 1e-3) / 1e6
+    h2d = C.sizeof(Scene) + C.sizeof(Sphere) * scene.s.n_spheres
+    if scene.s.sky_kind == 0 and scene.sky is not None:
+        h2d += scene.sky.nbytes
+    d2h = W * H * 3 if rank == 0 else 0
+
+    if rank != 0:
+        dist.barrier() if world > 1 else None
+        dist.destroy_process_group() if world > 1 else None
+        return 0
+
+    # ---- roofline of the dominant kernel (trace), FP64 pipe
+    peak = native.lib().bhrt_b200_fp64_peak_tflops(200000, 3, None)
+    avg_trace_ms = sum(trace_ms) / len(trace_ms)
+    achieved = (sum(flops) / len(flops)) / (avg_trace_ms * 1e-3) / 1e12
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(f"config{args.config}")
+        except Exception:
+            traffic = None
+
+    # ---- CPU baseline on this box's host cores (rank 0, N=1 only)
+    cpu = None
+    ref_sky = None
+    if world == 1 and not args.no_cpu:
+        threads = os.cpu_count() or 1
+        band = centre_band(H, args.cpu_rows)
+        rays, dt = cpu_port_rows(scene, band, threads)
+        cpu = {"value": rays / dt / 1e6, "unit": "Mrays/s", "cores": threads, "kind": "port",
+               "sample": f"oracle port (C, pthreads) of the full workload, centre rows "
+                         f"[{band[0]},{band[1]}) = {rays} rays, {dt:.1f} s"}
+        ref_sky = reference_sky_only(scene, args.ref_sky_rows, threads)
+
+    line = {
+        "metric": "Mrays/s", "value": value, "unit": "Mrays/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms_max,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": WORKLOADS[args.config], "width": W, "height": H, "spp": spp,
+                   "rays_per_step": total_rays,
+                   "l2": "flushed between steps (256 MiB write, outside the timed window)",
+                   "parallelism": f"cyclic rows x{world} + NCCL gather" if world > 1 else "1 GPU"},
+        "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "trace_scene_kernel" if scene.s.integrator else "trace_reference_kernel",
+                     "kernel_ms": avg_trace_ms, "shade_ms": sum(shade_ms) / len(shade_ms),
+                     "peak_source": "K0 fp64 FMA microbenchmark measured in this run "
+                                    "(MEASURED_PEAKS.json has no FP64 entry)",
+                     "flops_per_launch": sum(flops) / len(flops)},
+        "cpu_baseline": cpu,
+        "reference_sky_only": ref_sky,
+        "e2e": {"value": e2e_value, "unit": "Mrays/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "gpu_launches": stats["launches"] * args.steps if stats else None,
+        "gpu_launches_per_step": stats["launches"] if stats else None,
+        "steps_per_ray": stats["steps"] / stats["rays"] if stats else None,
+        "rejected_per_ray": stats["rejected"] / stats["rays"] if stats else None,
+        "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2, choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-rows", type=int, default=64)
+    ap.add_argument("--ref-rows", type=int, default=32)
+    ap.add_argument("--ref-sky-rows", type=int, default=2)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -212,6 +212,11 @@ int bhrt_ctx_finish(bhrt_ctx* ctx, bhrt_status_info* info);
  * rays, kernel launches. */
 int bhrt_ctx_stats(bhrt_ctx* ctx, uint64_t* steps, uint64_t* rejected, uint64_t* rays,
                    int32_t* launches);
+/* Per-kernel CUDA-event timing of subsequent renders (off by default).
+ * After bhrt_ctx_finish, bhrt_ctx_kernel_ms returns the durations of the
+ * last render's trace and shade kernels on the render stream. */
+int bhrt_ctx_set_timing(bhrt_ctx* ctx, int32_t enable);
+int bhrt_ctx_kernel_ms(bhrt_ctx* ctx, float* trace_ms, float* shade_ms);
 /* Number of rows selected by the tiling rule above. */
 int32_t bhrt_tile_row_count(int32_t row_start, int32_t row_end, int32_t tile_rows,
                             int32_t tile_stride, int32_t tile_offset);

@@ -658,6 +658,9 @@ typedef struct {
     const bhrt_scene* s;
     v3 O, e1, e2, n;
     double next_disk;  /* +inf when no disk events */
+    double disk_sigma; /* +1 / -1: which half of the disk line the next event is on */
+    double disk_lx, disk_ly; /* unit disk line in plane coordinates */
+    v3 disk_L;         /* unit disk line in world coordinates */
     int nc;            /* candidates (<= MAXC) or -1 = test all spheres every step */
     cand_t c[MAXC];
     double next_sph;
@@ -680,11 +683,19 @@ static void ray_events_setup(scene_ray_t* R) {
     const bhrt_scene* s = R->s;
     R->next_disk = INFINITY;
     if (s->disk_enabled) {
-        const v3 L = mk(-R->n.z, 0.0, R->n.x); /* n x (0,1,0) */
-        const double lx = dot(L, R->e1), ly = dot(L, R->e2);
-        if (norm(L) >= 1e-12) {
+        /* The disk plane (y = O.y) meets the orbital plane in the line
+         * through O along L = n x (0,1,0); crossings are the phi-events
+         * phi_L + k*pi. The hit direction alternates between +L^ and -L^. */
+        const v3 L = mk(-R->n.z, 0.0, R->n.x);
+        const double nl = norm(L);
+        if (nl >= 1e-12) {
+            const double lx = dot(L, R->e1), ly = dot(L, R->e2);
             const double pl = atan2(ly, lx);
             R->next_disk = pl > 0.0 ? pl : pl + PI;
+            R->disk_sigma = pl > 0.0 ? 1.0 : -1.0;
+            R->disk_lx = lx / nl;
+            R->disk_ly = ly / nl;
+            R->disk_L = dvd(L, nl);
         }
     }
     R->nc = 0;
@@ -716,14 +727,34 @@ static inline double hermite(double t, double h, double ua, double wa, double ub
     return h00 * ua + h10 * h * wa + h01 * ub + h11 * h * wb;
 }
 
-/* Polyline hit tests over the step (pa, ua, wa) -> (pb, ub, wb). Returns 1 on hit. */
+/* Hit tests over one accepted step (pa, ua, wa) -> (pb, ub, wb), DESIGN.md §Events.
+ *  - disk: exact phi-event; radius from the step's cubic Hermite interpolant of u;
+ *  - spheres: the step's polyline of S = ceil(h / chord_dphi) equal-angle
+ *    sub-chords (vertices: Hermite u, directions by a rotation recurrence),
+ *    first entering chord/circle intersection;
+ *  - both in one step: the one at the smaller orbital angle wins.
+ * Returns 1 on hit. */
 static int step_events(scene_ray_t* R, double pa, double ua, double wa, double pb, double ub,
                        double wb) {
     const bhrt_scene* s = R->s;
     const double h = pb - pa;
-    int S = 1;
-    if (h > s->chord_dphi) S = (int)ceil(h / s->chord_dphi);
-    /* active sphere candidates for this step */
+    int hit = 0;
+    /* ---- disk */
+    int disk_hit = 0;
+    double r_ev = 0.0, dlx = 0.0, dly = 0.0;
+    if (R->next_disk > pa && R->next_disk <= pb) {
+        const double t = (R->next_disk - pa) / h;
+        const double u_ev = hermite(t, h, ua, wa, ub, wb);
+        if (u_ev > 0.0) {
+            r_ev = 1.0 / u_ev;
+            if (r_ev >= s->disk_r_in && r_ev <= s->disk_r_out) {
+                disk_hit = 1;
+                dlx = R->disk_sigma * R->disk_lx;
+                dly = R->disk_sigma * R->disk_ly;
+            }
+        }
+    }
+    /* ---- spheres */
     int act[MAXC];
     int na = 0;
     cand_t all;
@@ -731,36 +762,24 @@ static int step_events(scene_ray_t* R, double pa, double ua, double wa, double p
     if (!test_all)
         for (int i = 0; i < R->nc; ++i)
             if (R->c[i].lo <= pb && R->c[i].hi >= pa) act[na++] = i;
-    const int disk_here = R->next_disk > pa && R->next_disk <= pb;
-    int hit = 0;
-    if (disk_here || na > 0 || test_all) {
-        double phj = pa, uj = ua;
-        double xj = cos(phj) / uj, yj = sin(phj) / uj;
-        for (int j = 0; j < S && !hit; ++j) {
-            double phk, uk;
-            if (j + 1 == S) { phk = pb; uk = ub; }
-            else {
-                const double t = (double)(j + 1) / S;
-                phk = pa + h * t;
-                uk = hermite(t, h, ua, wa, ub, wb);
-            }
-            const double xk = cos(phk) / uk, yk = sin(phk) / uk;
+    int sph_hit = 0, bsph = -1;
+    double bqx = 0.0, bqy = 0.0;
+    if (na > 0 || test_all) {
+        int S = 1;
+        if (h > s->chord_dphi) S = (int)ceil(h / s->chord_dphi);
+        const double dl = h / S;
+        const double cd_ = cos(dl), sd_ = sin(dl);
+        double cj = cos(pa), sj = sin(pa);
+        double rj = 1.0 / ua;
+        double xj = cj * rj, yj = sj * rj;
+        for (int j = 0; j < S && !sph_hit; ++j) {
+            const double ck = cj * cd_ - sj * sd_;
+            const double sk = sj * cd_ + cj * sd_;
+            const double uk = (j + 1 == S) ? ub : hermite((double)(j + 1) / S, h, ua, wa, ub, wb);
+            const double rk = 1.0 / uk;
+            const double xk = ck * rk, yk = sk * rk;
             const double dx = xk - xj, dy = yk - yj;
             double best = INFINITY;
-            int bobj = 0, bsph = -1;
-            double bqx = 0.0, bqy = 0.0;
-            if (disk_here && R->next_disk > phj && R->next_disk <= phk) {
-                const double lx = cos(R->next_disk), ly = sin(R->next_disk);
-                const double c0 = lx * yj - ly * xj;
-                const double c1 = lx * yk - ly * xk;
-                const double den = c0 - c1;
-                const double t = den != 0.0 ? c0 / den : 0.0;
-                const double qx = xj + t * dx, qy = yj + t * dy;
-                const double rq = sqrt(qx * qx + qy * qy);
-                if (rq >= s->disk_r_in && rq <= s->disk_r_out) {
-                    best = t; bobj = BHRT_OBJ_DISK; bqx = qx; bqy = qy;
-                }
-            }
             const int ncand = test_all ? s->n_spheres : na;
             for (int a = 0; a < ncand; ++a) {
                 const cand_t* cd;
@@ -784,21 +803,30 @@ static int step_events(scene_ray_t* R, double pa, double ua, double wa, double p
                 if (disc < 0.0) continue;
                 const double t = (-B - sqrt(disc)) / A;
                 if (t >= 0.0 && t <= 1.0 && t < best) {
-                    best = t; bobj = BHRT_OBJ_SPHERE; bsph = cd->k;
+                    best = t; sph_hit = 1; bsph = cd->k;
                     bqx = xj + t * dx; bqy = yj + t * dy;
                 }
             }
-            if (bobj) {
-                hit = 1;
-                R->obj = bobj;
-                R->sphere = bsph;
-                R->point = add(R->O, add(scl(R->e1, bqx), scl(R->e2, bqy)));
-            }
-            phj = phk; uj = uk; xj = xk; yj = yk;
+            cj = ck; sj = sk; xj = xk; yj = yk;
         }
     }
+    if (sph_hit && disk_hit) {
+        /* sphere point at a smaller angle than the disk line <=> cross(p, l) > 0 */
+        if (bqx * dly - bqy * dlx > 0.0) disk_hit = 0; else sph_hit = 0;
+    }
+    if (disk_hit) {
+        hit = 1;
+        R->obj = BHRT_OBJ_DISK;
+        R->sphere = -1;
+        R->point = add(R->O, scl(R->disk_L, R->disk_sigma * r_ev));
+    } else if (sph_hit) {
+        hit = 1;
+        R->obj = BHRT_OBJ_SPHERE;
+        R->sphere = bsph;
+        R->point = add(R->O, add(scl(R->e1, bqx), scl(R->e2, bqy)));
+    }
     /* advance event state past pb */
-    while (R->next_disk <= pb) R->next_disk += PI;
+    while (R->next_disk <= pb) { R->next_disk += PI; R->disk_sigma = -R->disk_sigma; }
     if (!test_all) {
         R->next_sph = INFINITY;
         for (int i = 0; i < R->nc; ++i) {

@@ -20,7 +20,7 @@
 
 namespace bhrt_b200 {
 
-int launch_trace(const KParams& p, cudaStream_t st, int* launches);
+int launch_trace(const KParams& p, cudaStream_t st, int* launches, cudaEvent_t* ev);
 
 namespace {
 
@@ -146,6 +146,9 @@ struct bhrt_ctx {
     int pending = 0;
     int32_t last_rows = 0;
     unsigned long long host_stats[4] = {0, 0, 0, 0};
+    bool timing = false;
+    bool timed = false;
+    cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
 };
 
 extern "C" {
@@ -270,8 +273,8 @@ double bhrt_flops_per_step(int32_t integrator) {
     // Algorithmic FP64 flops per accepted step, fma = 2.
     switch (integrator) {
         case BHRT_INTEGRATOR_REFERENCE: return 152.0;  // 110 stages + 38 error + 4 controller
-        case BHRT_INTEGRATOR_RK4: return 44.0;         // tests/oracles.hpp:23-30 op count
-        case BHRT_INTEGRATOR_RKF45: return 148.0;      // DESIGN.md §Roofline op count
+        case BHRT_INTEGRATOR_RK4: return 39.0;         // tests/oracles.hpp:23-30, invariants hoisted
+        case BHRT_INTEGRATOR_RKF45: return 137.0;      // DESIGN.md §Roofline op count
         default: return 0.0;
     }
 }
@@ -294,10 +297,34 @@ int bhrt_ctx_create(int32_t device, bhrt_ctx** out, bhrt_status_info* info) {
     return 0;
 }
 
+int bhrt_ctx_set_timing(bhrt_ctx* c, int32_t enable) {
+    if (!c) return BHRT_INVALID_ARGUMENT;
+    bhrt_status_info* info = nullptr;
+    CK(cudaSetDevice(c->device));
+    if (enable && !c->ev[0])
+        for (auto& e : c->ev) CK(cudaEventCreate(&e));
+    c->timing = enable != 0;
+    return 0;
+}
+
+int bhrt_ctx_kernel_ms(bhrt_ctx* c, float* trace_ms, float* shade_ms) {
+    if (!c || !c->timed || c->pending) return BHRT_INVALID_ARGUMENT;
+    bhrt_status_info* info = nullptr;
+    CK(cudaSetDevice(c->device));
+    float a = 0.f, b = 0.f;
+    CK(cudaEventElapsedTime(&a, c->ev[0], c->ev[1]));
+    CK(cudaEventElapsedTime(&b, c->ev[1], c->ev[2]));
+    if (trace_ms) *trace_ms = a;
+    if (shade_ms) *shade_ms = b;
+    return 0;
+}
+
 void bhrt_ctx_destroy(bhrt_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
+    for (auto& e : c->ev)
+        if (e) cudaEventDestroy(e);
     c->sky.release();
     c->spheres.release();
     c->tables.release();
@@ -411,7 +438,8 @@ int bhrt_ctx_render_async(bhrt_ctx* c, int32_t row_start, int32_t row_end, int32
     CK(cudaMemcpyAsync(c->stats.p, init, sizeof init, cudaMemcpyHostToDevice, st));
     CK(cudaMemsetAsync(c->queue.p, 0, sizeof(unsigned int), st));
     c->launches = 0;
-    if (rows > 0 && launch_trace(k, st, &c->launches) != 0)
+    c->timed = c->timing && rows > 0;
+    if (rows > 0 && launch_trace(k, st, &c->launches, c->timed ? c->ev : nullptr) != 0)
         return set_info(info, BHRT_INVALID_ARGUMENT, -1, -1, "render: unsupported integrator");
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(c->host_stats, c->stats.p, sizeof c->host_stats, cudaMemcpyDeviceToHost, st));

@@ -448,69 +448,89 @@ struct SphereSm {  // per-block staged sphere data, relative to the hole centre
     double cx[kMaxSpheres], cy[kMaxSpheres], cz[kMaxSpheres], r[kMaxSpheres];
 };
 
-struct Cand {
-    double cx, cy, rho2, lo, hi;
-    int k;
+// Per-thread sphere-candidate slots live in shared memory, lane-major
+// ([slot][thread]) so slot accesses are bank-conflict free. A slot holds the
+// sphere index and a CONSERVATIVE fp32 angular window: the window only decides
+// which steps run the exact fp64 hit test, so any superset of the oracle's
+// windows gives bit-identical results.
+constexpr int kBlock = 128;
+constexpr int kSlots = 8;
+constexpr float kWinMargin = 5e-4f;
+
+struct CandSm {
+    float lo[kSlots][kBlock];
+    float hi[kSlots][kBlock];
+    unsigned char k[kSlots][kBlock];
 };
 
 struct SceneRay {
     V3 O, e1, e2, n;
-    double next_disk, next_sph;
-    int nc;  // -1: test all spheres
-    Cand c[kMaxCand];
+    double next_disk;   // +inf: no disk events
+    double disk_sigma;  // +-1: half of the disk line of the next event
+    double disk_lx, disk_ly;
+    V3 disk_L;
+    float next_sph;     // min window start over slots (-inf: test all)
+    int nc;             // slots in use; -1: test every sphere every step
     int obj, sphere;
     V3 point;
 };
 
-__device__ __forceinline__ void sphere_window(double cx, double cy, double rho, double& lo, double& hi) {
-    const double rc = sqrt(cx * cx + cy * cy);
-    if (rc <= rho) {
-        lo = -CUDART_INF;
-        hi = CUDART_INF;
+__device__ __forceinline__ void sphere_window_f(double cx, double cy, double rho2, float& lo, float& hi) {
+    const double rc2 = cx * cx + cy * cy;
+    const double q = rc2 - rho2;  // rc^2 - rho^2
+    if (!(q > 0.0)) {
+        lo = -CUDART_INF_F;
+        hi = CUDART_INF_F;
         return;
     }
-    const double a = asin(rho / rc), pc = atan2(cy, cx);
-    const double m = 1e-9;
-    lo = pc - a - m;
-    hi = pc + a + m;
-    if (hi < 0.0) {
-        lo += 2.0 * PI_D;
-        hi += 2.0 * PI_D;
+    const float a = atan2f((float)sqrt(rho2), (float)sqrt(q));  // half-width asin(rho/rc)
+    const float pc = atan2f((float)cy, (float)cx);
+    lo = pc - a - kWinMargin;
+    hi = pc + a + kWinMargin;
+    if (hi < 0.0f) {
+        lo += 2.0f * (float)PI_D;
+        hi += 2.0f * (float)PI_D;
     }
 }
 
-__device__ void ray_events_setup(const KParams& p, const SphereSm& sm, SceneRay& R) {
+__device__ void ray_events_setup(const KParams& p, const SphereSm& sm, CandSm& cs, SceneRay& R) {
+    const int t = threadIdx.x;
     R.next_disk = CUDART_INF;
+    R.disk_sigma = 1.0;
     if (p.disk_enabled) {
         const V3 L = mk(-R.n.z, 0.0, R.n.x);
-        const double lx = dot(L, R.e1), ly = dot(L, R.e2);
-        if (norm(L) >= 1e-12) {
+        const double nl = norm(L);
+        if (nl >= 1e-12) {
+            const double lx = dot(L, R.e1), ly = dot(L, R.e2);
             const double pl = atan2(ly, lx);
             R.next_disk = pl > 0.0 ? pl : pl + PI_D;
+            R.disk_sigma = pl > 0.0 ? 1.0 : -1.0;
+            R.disk_lx = lx / nl;
+            R.disk_ly = ly / nl;
+            R.disk_L = dvd(L, nl);
         }
     }
     R.nc = 0;
-    R.next_sph = CUDART_INF;
+    R.next_sph = CUDART_INF_F;
     for (int k = 0; k < p.n_spheres; ++k) {
         const V3 c = mk(sm.cx[k], sm.cy[k], sm.cz[k]);
         const double dn = dot(c, R.n);
         if (!(fabs(dn) < sm.r[k])) continue;
-        if (R.nc == kMaxCand) {
+        if (R.nc == kSlots) {
             R.nc = -1;
             break;
         }
-        Cand& cd = R.c[R.nc++];
-        cd.k = k;
-        cd.cx = dot(c, R.e1);
-        cd.cy = dot(c, R.e2);
-        cd.rho2 = sm.r[k] * sm.r[k] - dn * dn;
-        sphere_window(cd.cx, cd.cy, sqrt(cd.rho2), cd.lo, cd.hi);
+        const double cx = dot(c, R.e1), cy = dot(c, R.e2);
+        const double rho2 = sm.r[k] * sm.r[k] - dn * dn;
+        float lo, hi;
+        sphere_window_f(cx, cy, rho2, lo, hi);
+        cs.lo[R.nc][t] = lo;
+        cs.hi[R.nc][t] = hi;
+        cs.k[R.nc][t] = (unsigned char)k;
+        R.next_sph = fminf(R.next_sph, lo);
+        ++R.nc;
     }
-    if (R.nc < 0) {
-        R.next_sph = -CUDART_INF;
-        return;
-    }
-    for (int i = 0; i < R.nc; ++i) R.next_sph = dmin(R.next_sph, R.c[i].lo);
+    if (R.nc < 0) R.next_sph = -CUDART_INF_F;
 }
 
 __device__ __forceinline__ double hermite(double t, double h, double ua, double wa, double ub, double wb) {
@@ -522,71 +542,70 @@ __device__ __forceinline__ double hermite(double t, double h, double ua, double 
     return h00 * ua + h10 * h * wa + h01 * ub + h11 * h * wb;
 }
 
-// Polyline hit tests over one step; mirrors oracle step_events().
-__device__ bool step_events(const KParams& p, const SphereSm& sm, SceneRay& R, double pa, double ua,
-                            double wa, double pb, double ub, double wb) {
+// Hit tests over one accepted step; mirrors oracle step_events() (same
+// operation order): disk = exact phi-event on the Hermite interpolant,
+// spheres = first entering hit on the step's equal-angle sub-chords.
+__device__ __forceinline__ bool step_events(const KParams& p, const SphereSm& sm, CandSm& cs, SceneRay& R,
+                                         double pa, double ua, double wa, double pb, double ub,
+                                         double wb) {
+    const int tid = threadIdx.x;
     const double h = pb - pa;
-    int S = 1;
-    if (h > p.chord_dphi) S = (int)ceil(h / p.chord_dphi);
+    // ---- disk
+    bool disk_hit = false;
+    double r_ev = 0.0, dlx = 0.0, dly = 0.0;
+    if (R.next_disk > pa && R.next_disk <= pb) {
+        const double t = (R.next_disk - pa) / h;
+        const double u_ev = hermite(t, h, ua, wa, ub, wb);
+        if (u_ev > 0.0) {
+            r_ev = 1.0 / u_ev;
+            if (r_ev >= p.disk_r_in && r_ev <= p.disk_r_out) {
+                disk_hit = true;
+                dlx = R.disk_sigma * R.disk_lx;
+                dly = R.disk_sigma * R.disk_ly;
+            }
+        }
+    }
+    // ---- spheres
     const bool test_all = R.nc < 0;
     unsigned act = 0;
-    if (!test_all)
+    if (!test_all) {
+        const float fa = (float)pa, fb = (float)pb;
         for (int i = 0; i < R.nc; ++i)
-            if (R.c[i].lo <= pb && R.c[i].hi >= pa) act |= 1u << i;
-    const bool disk_here = R.next_disk > pa && R.next_disk <= pb;
-    bool hit = false;
-    if (disk_here || act || test_all) {
-        double phj = pa, uj = ua;
-        double xj = cos(phj) / uj, yj = sin(phj) / uj;
-        for (int j = 0; j < S && !hit; ++j) {
-            double phk, uk;
-            if (j + 1 == S) {
-                phk = pb;
-                uk = ub;
-            } else {
-                const double t = (double)(j + 1) / S;
-                phk = pa + h * t;
-                uk = hermite(t, h, ua, wa, ub, wb);
-            }
-            const double xk = cos(phk) / uk, yk = sin(phk) / uk;
+            if (cs.lo[i][tid] <= fb && cs.hi[i][tid] >= fa) act |= 1u << i;
+    }
+    bool sph_hit = false;
+    int bsph = -1;
+    double bqx = 0.0, bqy = 0.0;
+    if (act || test_all) {
+        int S = 1;
+        if (h > p.chord_dphi) S = (int)ceil(h / p.chord_dphi);
+        const double dl = h / S;
+        const double cd_ = cos(dl), sd_ = sin(dl);
+        double cj = cos(pa), sj = sin(pa);
+        const double rj = 1.0 / ua;
+        double xj = cj * rj, yj = sj * rj;
+        for (int j = 0; j < S && !sph_hit; ++j) {
+            const double ck = cj * cd_ - sj * sd_;
+            const double sk = sj * cd_ + cj * sd_;
+            const double uk = (j + 1 == S) ? ub : hermite((double)(j + 1) / S, h, ua, wa, ub, wb);
+            const double rk = 1.0 / uk;
+            const double xk = ck * rk, yk = sk * rk;
             const double dx = xk - xj, dy = yk - yj;
             double best = CUDART_INF;
-            int bobj = 0, bsph = -1;
-            double bqx = 0.0, bqy = 0.0;
-            if (disk_here && R.next_disk > phj && R.next_disk <= phk) {
-                const double lx = cos(R.next_disk), ly = sin(R.next_disk);
-                const double c0 = lx * yj - ly * xj;
-                const double c1 = lx * yk - ly * xk;
-                const double den = c0 - c1;
-                const double t = den != 0.0 ? c0 / den : 0.0;
-                const double qx = xj + t * dx, qy = yj + t * dy;
-                const double rq = sqrt(qx * qx + qy * qy);
-                if (rq >= p.disk_r_in && rq <= p.disk_r_out) {
-                    best = t;
-                    bobj = BHRT_OBJ_DISK;
-                    bqx = qx;
-                    bqy = qy;
-                }
-            }
             const int ncand = test_all ? p.n_spheres : R.nc;
             for (int a = 0; a < ncand; ++a) {
-                double ccx, ccy, rho2;
                 int k;
                 if (test_all) {
-                    const V3 c = mk(sm.cx[a], sm.cy[a], sm.cz[a]);
-                    const double dn = dot(c, R.n);
-                    if (!(fabs(dn) < sm.r[a])) continue;
                     k = a;
-                    ccx = dot(c, R.e1);
-                    ccy = dot(c, R.e2);
-                    rho2 = sm.r[a] * sm.r[a] - dn * dn;
                 } else {
                     if (!(act & (1u << a))) continue;
-                    k = R.c[a].k;
-                    ccx = R.c[a].cx;
-                    ccy = R.c[a].cy;
-                    rho2 = R.c[a].rho2;
+                    k = cs.k[a][tid];
                 }
+                const V3 c = mk(sm.cx[k], sm.cy[k], sm.cz[k]);
+                const double dn = dot(c, R.n);
+                if (!(fabs(dn) < sm.r[k])) continue;
+                const double ccx = dot(c, R.e1), ccy = dot(c, R.e2);
+                const double rho2 = sm.r[k] * sm.r[k] - dn * dn;
                 const double mx = xj - ccx, my = yj - ccy;
                 const double A = dx * dx + dy * dy;
                 const double Bq = mx * dx + my * dy;
@@ -597,33 +616,56 @@ __device__ bool step_events(const KParams& p, const SphereSm& sm, SceneRay& R, d
                 const double t = (-Bq - sqrt(disc)) / A;
                 if (t >= 0.0 && t <= 1.0 && t < best) {
                     best = t;
-                    bobj = BHRT_OBJ_SPHERE;
+                    sph_hit = true;
                     bsph = k;
                     bqx = xj + t * dx;
                     bqy = yj + t * dy;
                 }
             }
-            if (bobj) {
-                hit = true;
-                R.obj = bobj;
-                R.sphere = bsph;
-                R.point = add(R.O, add(scl(R.e1, bqx), scl(R.e2, bqy)));
-            }
-            phj = phk;
-            uj = uk;
+            cj = ck;
+            sj = sk;
             xj = xk;
             yj = yk;
         }
     }
-    while (R.next_disk <= pb) R.next_disk += PI_D;
+    if (sph_hit && disk_hit) {
+        if (bqx * dly - bqy * dlx > 0.0)
+            disk_hit = false;
+        else
+            sph_hit = false;
+    }
+    bool hit = false;
+    if (disk_hit) {
+        hit = true;
+        R.obj = BHRT_OBJ_DISK;
+        R.sphere = -1;
+        R.point = add(R.O, scl(R.disk_L, R.disk_sigma * r_ev));
+    } else if (sph_hit) {
+        hit = true;
+        R.obj = BHRT_OBJ_SPHERE;
+        R.sphere = bsph;
+        R.point = add(R.O, add(scl(R.e1, bqx), scl(R.e2, bqy)));
+    }
+    while (R.next_disk <= pb) {
+        R.next_disk += PI_D;
+        R.disk_sigma = -R.disk_sigma;
+    }
     if (!test_all) {
-        R.next_sph = CUDART_INF;
+        R.next_sph = CUDART_INF_F;
+        const float fb = (float)pb;
         for (int i = 0; i < R.nc; ++i) {
-            while (R.c[i].hi < pb) {
-                R.c[i].lo += 2.0 * PI_D;
-                R.c[i].hi += 2.0 * PI_D;
+            float lo = cs.lo[i][tid], hi = cs.hi[i][tid];
+            bool moved = false;
+            while (hi < fb) {
+                lo += 2.0f * (float)PI_D;
+                hi += 2.0f * (float)PI_D;
+                moved = true;
             }
-            R.next_sph = dmin(R.next_sph, R.c[i].lo);
+            if (moved) {
+                cs.lo[i][tid] = lo;
+                cs.hi[i][tid] = hi;
+            }
+            R.next_sph = fminf(R.next_sph, lo);
         }
     }
     return hit;
@@ -670,9 +712,10 @@ __device__ void radial_scene(const KParams& p, const SphereSm& sm, SceneRay& R, 
 }
 
 template <int INTEG>
-__global__ void __launch_bounds__(128) trace_scene_kernel(const KParams p) {
+__global__ void __launch_bounds__(kBlock) trace_scene_kernel(const KParams p) {
     __shared__ SphereSm sm;
     __shared__ double s_grow[kQN], s_shrink[kQN];
+    __shared__ CandSm cs;
     for (int k = threadIdx.x; k < p.n_spheres; k += blockDim.x) {
         const bhrt_sphere sp = p.spheres[k];
         sm.cx[k] = sp.center[0] - p.center[0];
@@ -714,7 +757,7 @@ __global__ void __launch_bounds__(128) trace_scene_kernel(const KParams p) {
             R.n = cross(R.e1, R.e2);
             double u, w;
             initial_conditions(origin, dir, R.O, u, w);
-            ray_events_setup(p, sm, R);
+            ray_events_setup(p, sm, cs, R);
             if (INTEG == BHRT_INTEGRATOR_RK4) {
                 const double h = p.step;
                 for (;;) {
@@ -729,7 +772,7 @@ __global__ void __launch_bounds__(128) trace_scene_kernel(const KParams p) {
                     rk4_step(u, w, h, p.mass, un, wn);
                     const double pn = phi + h;
                     ++nsteps;
-                    if (pn >= dmin(R.next_disk, R.next_sph) && step_events(p, sm, R, phi, u, w, pn, un, wn)) {
+                    if (pn >= dmin(R.next_disk, R.next_sph) && step_events(p, sm, cs, R, phi, u, w, pn, un, wn)) {
                         phi = pn;
                         break;
                     }
@@ -752,7 +795,7 @@ __global__ void __launch_bounds__(128) trace_scene_kernel(const KParams p) {
                     if (rkf45_step(u, w, h, p.M3, p.rel_tol, p.abs_tol, p.max_step, s_grow, s_shrink, un, wn, hn)) {
                         const double pn = phi + h;
                         ++nsteps;
-                        if (pn >= dmin(R.next_disk, R.next_sph) && step_events(p, sm, R, phi, u, w, pn, un, wn)) {
+                        if (pn >= dmin(R.next_disk, R.next_sph) && step_events(p, sm, cs, R, phi, u, w, pn, un, wn)) {
                             phi = pn;
                             break;
                         }
@@ -887,10 +930,11 @@ __global__ void __launch_bounds__(256) shade_kernel(const KParams p) {
 }
 
 // ----------------------------------------------------------------- launch wrappers
-int launch_trace(const KParams& p, cudaStream_t st, int* launches) {
+int launch_trace(const KParams& p, cudaStream_t st, int* launches, cudaEvent_t* ev) {
     const long long n = (long long)p.n_rows * p.width * p.spp;
     if (n <= 0) return 0;
     const int threads = 128;
+    if (ev) cudaEventRecord(ev[0], st);
     const long long blocks = (n + threads - 1) / threads;
     switch (p.integrator) {
         case BHRT_INTEGRATOR_REFERENCE:
@@ -906,9 +950,11 @@ int launch_trace(const KParams& p, cudaStream_t st, int* launches) {
             return -1;
     }
     ++*launches;
+    if (ev) cudaEventRecord(ev[1], st);
     const long long npix = (long long)p.n_rows * p.width;
     shade_kernel<<<(unsigned)((npix + 255) / 256), 256, 0, st>>>(p);
     ++*launches;
+    if (ev) cudaEventRecord(ev[2], st);
     return 0;
 }
 

@@ -163,6 +163,17 @@ class Context:
         info = StatusInfo()
         _raise(native.lib().bhrt_ctx_finish(self._h, C.byref(info)), info)
 
+    def set_timing(self, enable: bool = True):
+        native.lib().bhrt_ctx_set_timing(self._h, 1 if enable else 0)
+
+    def kernel_ms(self) -> tuple[float, float]:
+        """(trace_ms, shade_ms) of the last finished render (set_timing first)."""
+        a, b = C.c_float(), C.c_float()
+        rc = native.lib().bhrt_ctx_kernel_ms(self._h, C.byref(a), C.byref(b))
+        if rc:
+            raise native.BhrtError(rc, -1, -1, "kernel timing unavailable")
+        return a.value, b.value
+
     def stats(self) -> dict:
         st, rj, rays = C.c_uint64(), C.c_uint64(), C.c_uint64()
         ln = C.c_int32()

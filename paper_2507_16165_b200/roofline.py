@@ -1,0 +1,35 @@
+"""Algorithmic FP64 flop accounting for the roofline.
+
+Counts are per the normative operation order of the kernels (= the oracle):
+an fma is 2 flops, every other +,-,*,/,sqrt is 1; transcendentals
+(sin/cos/atan2/asin/pow), comparisons, fabs/fmin/fmax and integer work are 0.
+Loop invariants (3M, h/2, h/6) are counted once per ray, i.e. not per step.
+
+per step attempt (accepted or rejected):
+  RKF45     137  = 6 rhs x 3 + stage sums 70 + 5th-order 22 + error 20
+                   + scales 4 + guard 1 + h update 1 + phi update 1
+  RK4        39  = 4 rhs x 3 + stage inputs 12 + combination 14 + phi 1
+  REFERENCE 152  = DOPRI5 step incl. error norm and PI control
+per ray (scene modes): camera ray 31 + plane basis 38 + initial
+  conditions 33 + plane normal 9 + disk line 16 + sphere cull 5/sphere.
+Event (polyline hit-test) and shading arithmetic are not counted, so the
+achieved figure is a lower bound.
+"""
+from __future__ import annotations
+
+from .abi import INTEGRATOR_REFERENCE, INTEGRATOR_RK4, INTEGRATOR_RKF45
+
+STEP_FLOPS = {INTEGRATOR_RKF45: 137.0, INTEGRATOR_RK4: 39.0, INTEGRATOR_REFERENCE: 152.0}
+
+
+def setup_flops(scene) -> float:
+    s = scene.s if hasattr(scene, "s") else scene
+    if s.integrator == INTEGRATOR_REFERENCE:
+        return 31.0 + 38.0 + 33.0
+    return 31.0 + 38.0 + 33.0 + 9.0 + (16.0 if s.disk_enabled else 0.0) + 5.0 * s.n_spheres
+
+
+def launch_flops(scene, stats: dict) -> float:
+    s = scene.s if hasattr(scene, "s") else scene
+    attempts = stats["steps"] + stats["rejected"]
+    return attempts * STEP_FLOPS[s.integrator] + stats["rays"] * setup_flops(scene)
