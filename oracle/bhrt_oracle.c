@@ -844,6 +844,40 @@ static v3 tangent_dir(const scene_ray_t* R, double phi, double u, double w) {
     return normalized(add(scl(R->e1, tx), scl(R->e2, ty)));
 }
 
+/* d/dt of hermite() (t in [0,1]); h01' = -h00'. */
+static inline double hermite_d(double t, double h, double ua, double wa, double ub, double wb) {
+    const double t2 = t * t;
+    const double d00 = 6.0 * t2 - 6.0 * t;
+    const double d10 = 3.0 * t2 - 4.0 * t + 1.0;
+    const double d11 = 3.0 * t2 - 2.0 * t;
+    return d00 * ua + d10 * h * wa - d00 * ub + d11 * h * wb;
+}
+
+/* Escape direction: the tangent where the trajectory
+ * crosses r = escape_radius inside the last step, located on the step's
+ * Hermite interpolant (linear guess + 2 Newton iterations), so the
+ * direction does not depend on how far the last step overshot. Without a
+ * crossing step (ray starts beyond the escape radius) it is the tangent at
+ * the current state. */
+static v3 escape_dir(const scene_ray_t* R, int has_step, double pa, double ua, double wa, double pb,
+                     double ub, double wb, double u_esc, double energy, double M2) {
+    if (!has_step || !(ua > u_esc)) return tangent_dir(R, pb, ub, wb);
+    const double h = pb - pa;
+    double t = (ua - u_esc) / (ua - ub);
+    for (int it = 0; it < 2; ++it) {
+        const double f = hermite(t, h, ua, wa, ub, wb) - u_esc;
+        const double df = hermite_d(t, h, ua, wa, ub, wb);
+        if (df != 0.0) t = t - f / df;
+        t = clampd(t, 0.0, 1.0);
+    }
+    const double us = hermite(t, h, ua, wa, ub, wb);
+    /* u' from the first integral u'^2 = E - u^2 + 2Mu^3 (geodesic.cpp:272-275),
+     * outgoing branch: more accurate than the interpolant's derivative. */
+    const double q = energy - us * us + M2 * us * us * us;
+    const double ws = -sqrt(q > 0.0 ? q : 0.0);
+    return tangent_dir(R, pa + h * t, us, ws);
+}
+
 /* Radial ray in a scene: straight segment (geodesic.cpp:175-187) with hit tests. */
 static void radial_scene(scene_ray_t* R, v3 origin, v3 dir, double seg_len, int captured) {
     const bhrt_scene* s = R->s;
@@ -897,12 +931,20 @@ static int trace_scene(const bhrt_scene* s, const prep_t* P, v3 origin, v3 dir, 
     orc_initial_conditions(o, d, s->center, st);
     ray_events_setup(R);
     double phi = 0.0, u = st[1], w = st[2];
+    double pp = 0.0, up = 0.0, wp = 0.0; /* state before the last accepted step */
+    int has_step = 0;
+    const double M2 = 2.0 * s->mass;
+    const double energy = w * w + u * u - M2 * u * u * u; /* conserved_energy, geodesic.cpp:272-275 */
     if (s->integrator == BHRT_INTEGRATOR_RK4) {
         const double h = s->step;
         for (;;) { /* oracles.hpp:47-54 loop structure */
             if (!(phi < P->phi_max)) { R->obj = BHRT_OBJ_STALLED; break; }
             if (u >= P->u_cap) { R->obj = BHRT_OBJ_HORIZON; break; }
-            if (u <= P->u_esc && w < 0.0) { R->obj = BHRT_OBJ_SKY; R->point = tangent_dir(R, phi, u, w); break; }
+            if (u <= P->u_esc && w < 0.0) {
+                R->obj = BHRT_OBJ_SKY;
+                R->point = escape_dir(R, has_step, pp, up, wp, phi, u, w, P->u_esc, energy, M2);
+                break;
+            }
             double nx[2];
             orc_rk4_step(u, w, h, s->mass, nx);
             const double pn = phi + h;
@@ -911,6 +953,7 @@ static int trace_scene(const bhrt_scene* s, const prep_t* P, v3 origin, v3 dir, 
                 phi = pn;
                 break;
             }
+            pp = phi; up = u; wp = w; has_step = 1;
             phi = pn; u = nx[0]; w = nx[1];
             if (!(u > 0.0)) return BHRT_NUMERICAL;
         }
@@ -918,7 +961,11 @@ static int trace_scene(const bhrt_scene* s, const prep_t* P, v3 origin, v3 dir, 
         double h = s->step;
         for (;;) { /* geodesic.cpp:199-236 loop structure */
             if (u >= P->u_cap) { R->obj = BHRT_OBJ_HORIZON; break; }
-            if (u <= P->u_esc && w < 0.0) { R->obj = BHRT_OBJ_SKY; R->point = tangent_dir(R, phi, u, w); break; }
+            if (u <= P->u_esc && w < 0.0) {
+                R->obj = BHRT_OBJ_SKY;
+                R->point = escape_dir(R, has_step, pp, up, wp, phi, u, w, P->u_esc, energy, M2);
+                break;
+            }
             if (phi > P->phi_max) { R->obj = BHRT_OBJ_STALLED; break; }
             double un, wn, hn;
             const int acc = rkf45_step(u, w, h, P->M3, s->rel_tol, s->abs_tol, s->max_step, &un, &wn, &hn);
@@ -929,6 +976,7 @@ static int trace_scene(const bhrt_scene* s, const prep_t* P, v3 origin, v3 dir, 
                     phi = pn;
                     break;
                 }
+                pp = phi; up = u; wp = w; has_step = 1;
                 phi = pn; u = un; w = wn;
                 if (!(u > 0.0)) return BHRT_NUMERICAL;
             } else {

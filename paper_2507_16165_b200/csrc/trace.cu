@@ -677,6 +677,34 @@ __device__ __forceinline__ V3 tangent_dir(const SceneRay& R, double phi, double 
     return normalized(add(scl(R.e1, tx), scl(R.e2, ty)));
 }
 
+__device__ __forceinline__ double hermite_d(double t, double h, double ua, double wa, double ub,
+                                            double wb) {
+    const double t2 = t * t;
+    const double d00 = 6.0 * t2 - 6.0 * t;
+    const double d10 = 3.0 * t2 - 4.0 * t + 1.0;
+    const double d11 = 3.0 * t2 - 2.0 * t;
+    return d00 * ua + d10 * h * wa - d00 * ub + d11 * h * wb;
+}
+
+// Tangent at the r = escape_radius crossing of the last step (oracle escape_dir).
+__device__ __forceinline__ V3 escape_dir(const SceneRay& R, bool has_step, double pa, double ua, double wa,
+                                      double pb, double ub, double wb, double u_esc, double energy,
+                                      double M2) {
+    if (!has_step || !(ua > u_esc)) return tangent_dir(R, pb, ub, wb);
+    const double h = pb - pa;
+    double t = (ua - u_esc) / (ua - ub);
+    for (int it = 0; it < 2; ++it) {
+        const double f = hermite(t, h, ua, wa, ub, wb) - u_esc;
+        const double df = hermite_d(t, h, ua, wa, ub, wb);
+        if (df != 0.0) t = t - f / df;
+        t = clampd(t, 0.0, 1.0);
+    }
+    const double us = hermite(t, h, ua, wa, ub, wb);
+    const double q = energy - us * us + M2 * us * us * us;
+    const double ws = -sqrt(q > 0.0 ? q : 0.0);
+    return tangent_dir(R, pa + h * t, us, ws);
+}
+
 __device__ void radial_scene(const KParams& p, const SphereSm& sm, SceneRay& R, V3 origin, V3 dir,
                              double seg_len, bool captured) {
     double best = seg_len;
@@ -758,6 +786,10 @@ __global__ void __launch_bounds__(kBlock) trace_scene_kernel(const KParams p) {
             double u, w;
             initial_conditions(origin, dir, R.O, u, w);
             ray_events_setup(p, sm, cs, R);
+            double pp = 0.0, up = 0.0, wp = 0.0;  // state before the last accepted step
+            bool has_step = false;
+            const double M2 = 2.0 * p.mass;
+            const double energy = w * w + u * u - M2 * u * u * u;
             if (INTEG == BHRT_INTEGRATOR_RK4) {
                 const double h = p.step;
                 for (;;) {
@@ -765,7 +797,6 @@ __global__ void __launch_bounds__(kBlock) trace_scene_kernel(const KParams p) {
                     if (u >= p.u_cap) { R.obj = BHRT_OBJ_HORIZON; break; }
                     if (u <= p.u_esc && w < 0.0) {
                         R.obj = BHRT_OBJ_SKY;
-                        R.point = tangent_dir(R, phi, u, w);
                         break;
                     }
                     double un, wn;
@@ -776,6 +807,10 @@ __global__ void __launch_bounds__(kBlock) trace_scene_kernel(const KParams p) {
                         phi = pn;
                         break;
                     }
+                    pp = phi;
+                    up = u;
+                    wp = w;
+                    has_step = true;
                     phi = pn;
                     u = un;
                     w = wn;
@@ -787,7 +822,6 @@ __global__ void __launch_bounds__(kBlock) trace_scene_kernel(const KParams p) {
                     if (u >= p.u_cap) { R.obj = BHRT_OBJ_HORIZON; break; }
                     if (u <= p.u_esc && w < 0.0) {
                         R.obj = BHRT_OBJ_SKY;
-                        R.point = tangent_dir(R, phi, u, w);
                         break;
                     }
                     if (phi > p.phi_max) { R.obj = BHRT_OBJ_STALLED; break; }
@@ -799,6 +833,10 @@ __global__ void __launch_bounds__(kBlock) trace_scene_kernel(const KParams p) {
                             phi = pn;
                             break;
                         }
+                        pp = phi;
+                        up = u;
+                        wp = w;
+                        has_step = true;
                         phi = pn;
                         u = un;
                         w = wn;
@@ -813,6 +851,8 @@ __global__ void __launch_bounds__(kBlock) trace_scene_kernel(const KParams p) {
                     }
                 }
             }
+            if (R.obj == BHRT_OBJ_SKY)
+                R.point = escape_dir(R, has_step, pp, up, wp, phi, u, w, p.u_esc, energy, M2);
         }
         rec.object = R.obj;
         rec.sphere = R.sphere;

@@ -1,0 +1,114 @@
+"""The C-ABI library without a GPU: it loads, exports every symbol
+include/bhrt_cuda.h declares, its structs match the C compiler's layout,
+and the host-only entry points (defaults, validation, bands, tiling,
+sphere field) behave like the reference / the oracle."""
+import ctypes as C
+import os
+import re
+import subprocess
+import textwrap
+
+import numpy as np
+import pytest
+
+from oracle_lib import oracle
+from paper_2507_16165_b200 import native, scenes
+from paper_2507_16165_b200.abi import RayRecord, Scene, Sphere, StatusInfo
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "bhrt_cuda.h")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(bhrt_\w+)\s*\(", src)) - {"bhrt_status", "bhrt_ctx"})
+
+
+def test_library_loads_and_exports_every_declared_symbol():
+    L = native.lib()
+    names = declared_functions()
+    assert len(names) >= 15
+    for n in names:
+        assert hasattr(L, n), n
+    assert set(names) <= set(native.EXPORTS) | {"bhrt_cuda_abi_version"}
+    assert L.bhrt_cuda_abi_version() == 1
+
+
+def test_struct_layout_matches_c(tmp_path):
+    fields = [f for f, _ in Scene._fields_]
+    prog = ["#include <stdio.h>", "#include <stddef.h>", f'#include "{HEADER}"', "int main(void){"]
+    prog.append('printf("%zu %zu %zu %zu\\n", sizeof(bhrt_scene), sizeof(bhrt_sphere), '
+                'sizeof(bhrt_ray_record), sizeof(bhrt_status_info));')
+    for f in fields:
+        prog.append(f'printf("%zu\\n", offsetof(bhrt_scene, {f}));')
+    prog.append("return 0;}")
+    c = tmp_path / "probe.c"
+    c.write_text("\n".join(prog))
+    exe = tmp_path / "probe"
+    subprocess.run(["gcc", "-o", str(exe), str(c)], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()
+    assert [int(x) for x in out[:4]] == [C.sizeof(Scene), C.sizeof(Sphere), C.sizeof(RayRecord),
+                                        C.sizeof(StatusInfo)]
+    for f, off in zip(fields, out[4:]):
+        assert getattr(Scene, f).offset == int(off), f
+
+
+def test_defaults_agree_python_c_oracle():
+    a, b, c = Scene(), Scene(), Scene()
+    scenes.scene_defaults(a)
+    native.lib().bhrt_scene_defaults(C.byref(b))
+    oracle().orc_scene_defaults(C.byref(c))
+    assert bytes(a) == bytes(b) == bytes(c)
+
+
+def test_validation_codes_without_gpu():
+    L = native.lib()
+    info = StatusInfo()
+    sb = scenes.small_scene(scenes.gradient_background(), 4)
+    assert L.bhrt_validate_scene(sb.ptr(), C.byref(info)) == 0
+    for mutate in (lambda s: setattr(s.s, "spp", 0), lambda s: setattr(s.s, "width", 0),
+                   lambda s: s.set(cam_pos=(0, 0, -1.5)), lambda s: s.set_sky(None),
+                   lambda s: setattr(s.s, "mass", -1.0)):
+        bad = sb.clone()
+        mutate(bad)
+        assert L.bhrt_validate_scene(bad.ptr(), C.byref(info)) == 1
+        assert info.code == 1 and info.message
+
+
+def test_bands_and_tiles():
+    L = native.lib()
+    o = oracle()
+    rng = np.random.default_rng(1)
+    for _ in range(200):
+        h, w = int(rng.integers(1, 3000)), int(rng.integers(1, 64))
+        n = min(h, w)
+        a0, a1, b0, b1 = ((C.c_int32 * n)() for _ in range(4))
+        ca, cb = C.c_int32(), C.c_int32()
+        assert L.bhrt_make_bands(h, w, a0, a1, n, C.byref(ca)) == 0
+        assert o.orc_make_bands(h, w, b0, b1, n, C.byref(cb)) == 0
+        assert list(a0) == list(b0) and list(a1) == list(b1)
+        # cyclic tiles: counts partition the rows
+        T = int(rng.integers(1, 9))
+        assert sum(L.bhrt_tile_row_count(0, h, T, w, r) for r in range(w)) == h
+    assert L.bhrt_tile_row_count(0, 10, 0, 1, 0) == -1
+    assert L.bhrt_make_bands(0, 3, a0, a1, 3, C.byref(ca)) == 6
+
+
+def test_sphere_field_identical_to_oracle():
+    a = scenes.make_spheres()
+    b = scenes.make_spheres(lib=oracle())
+    assert bytes((Sphere * 64)(*a)) == bytes((Sphere * 64)(*b))
+
+
+def test_render_without_device_fails_loudly():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    sb = scenes.config(1, 8, 8)
+    out = np.zeros(8 * 8 * 3, np.uint8)
+    info = StatusInfo()
+    rc = native.lib().bhrt_cuda_render_rows(sb.ptr(), 0, 8, None, 0,
+                                            out.ctypes.data_as(C.POINTER(C.c_uint8)), out.nbytes,
+                                            None, C.byref(info))
+    assert rc == 5  # BHRT_DEVICE: no silent CPU fallback
