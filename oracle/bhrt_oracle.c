@@ -718,13 +718,24 @@ static void ray_events_setup(scene_ray_t* R) {
 }
 
 /* Cubic Hermite interpolation of u over one step, t in [0,1]. */
+/* Monomial coefficients of the cubic Hermite interpolant of u over a step of
+ * size h (u(0)=ua, u'(0)=h*wa, u(1)=ub, u'(1)=h*wb), normative op order. */
+static inline void hermite_coef(double h, double ua, double wa, double ub, double wb, double a[4]) {
+    a[0] = ua;
+    a[1] = h * wa;
+    a[2] = 3.0 * (ub - ua) - h * (2.0 * wa + wb);
+    a[3] = 2.0 * (ua - ub) + h * (wa + wb);
+}
+static inline double hermite_eval(const double a[4], double t) {
+    return fma(fma(fma(a[3], t, a[2]), t, a[1]), t, a[0]);
+}
+static inline double hermite_deval(const double a[4], double t) { /* d/dt */
+    return fma(fma(3.0 * a[3], t, 2.0 * a[2]), t, a[1]);
+}
 static inline double hermite(double t, double h, double ua, double wa, double ub, double wb) {
-    const double t2 = t * t, omt = 1.0 - t;
-    const double h00 = (1.0 + 2.0 * t) * omt * omt;
-    const double h10 = t * omt * omt;
-    const double h01 = t2 * (3.0 - 2.0 * t);
-    const double h11 = t2 * (t - 1.0);
-    return h00 * ua + h10 * h * wa + h01 * ub + h11 * h * wb;
+    double a[4];
+    hermite_coef(h, ua, wa, ub, wb, a);
+    return hermite_eval(a, t);
 }
 
 /* Hit tests over one accepted step (pa, ua, wa) -> (pb, ub, wb), DESIGN.md §Events.
@@ -846,11 +857,9 @@ static v3 tangent_dir(const scene_ray_t* R, double phi, double u, double w) {
 
 /* d/dt of hermite() (t in [0,1]); h01' = -h00'. */
 static inline double hermite_d(double t, double h, double ua, double wa, double ub, double wb) {
-    const double t2 = t * t;
-    const double d00 = 6.0 * t2 - 6.0 * t;
-    const double d10 = 3.0 * t2 - 4.0 * t + 1.0;
-    const double d11 = 3.0 * t2 - 2.0 * t;
-    return d00 * ua + d10 * h * wa - d00 * ub + d11 * h * wb;
+    double a[4];
+    hermite_coef(h, ua, wa, ub, wb, a);
+    return hermite_deval(a, t);
 }
 
 /* Escape direction: the tangent where the trajectory

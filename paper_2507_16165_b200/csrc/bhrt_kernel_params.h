@@ -6,7 +6,7 @@
 
 #include <cstdint>
 
-#include "../../include/bhrt_cuda.h"
+#include "bhrt_cuda.h"
 
 namespace bhrt_b200 {
 

@@ -1,0 +1,287 @@
+// device_common.cuh — device helpers shared by the trace kernels.
+//
+// Everything here follows the reference's operation order (vec3.hpp:7-44,
+// camera.cpp:10-68, geodesic.cpp:49-65) or the normative order of the
+// oracle (oracle/bhrt_oracle.c) for the extensions; the kernels are compiled
+// with --fmad=false so only the fma() calls written out below are fused.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <math_constants.h>
+
+#include <cstdint>
+
+#include "bhrt_kernel_params.h"
+
+namespace bhrt_b200 {
+
+#define PI_D 3.141592653589793
+
+// ----------------------------------------------------------------- vec3 (vec3.hpp:7-44 order)
+struct V3 {
+    double x, y, z;
+};
+__device__ __forceinline__ V3 mk(double x, double y, double z) { return {x, y, z}; }
+__device__ __forceinline__ V3 vld(const double* a) { return {a[0], a[1], a[2]}; }
+__device__ __forceinline__ V3 add(V3 a, V3 b) { return {a.x + b.x, a.y + b.y, a.z + b.z}; }
+__device__ __forceinline__ V3 sub(V3 a, V3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+__device__ __forceinline__ V3 scl(V3 a, double s) { return {a.x * s, a.y * s, a.z * s}; }
+__device__ __forceinline__ V3 dvd(V3 a, double s) { return {a.x / s, a.y / s, a.z / s}; }
+__device__ __forceinline__ double dot(V3 a, V3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+__device__ __forceinline__ V3 cross(V3 a, V3 b) {
+    return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+}
+__device__ __forceinline__ double norm(V3 a) { return sqrt(dot(a, a)); }
+__device__ __forceinline__ V3 normalized(V3 a) {
+    const double n = norm(a);
+    return {a.x / n, a.y / n, a.z / n};
+}
+__device__ __forceinline__ double clampd(double v, double lo, double hi) {
+    return v < lo ? lo : (hi < v ? hi : v);
+}
+__device__ __forceinline__ double dmax(double a, double b) { return a < b ? b : a; }
+__device__ __forceinline__ double dmin(double a, double b) { return b < a ? b : a; }
+
+// ----------------------------------------------------------------- camera (camera.cpp:10-68)
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+    x += 0x9e3779b97f4a7c15ULL;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+    return x ^ (x >> 31);
+}
+__device__ __forceinline__ double to_unit(uint64_t h) { return (double)(h >> 11) * 0x1.0p-53; }
+__device__ __forceinline__ uint64_t hash_counter(uint64_t seed, uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t h = splitmix64(seed);
+    h = splitmix64(h ^ a);
+    h = splitmix64(h ^ b);
+    h = splitmix64(h ^ c);
+    return h;
+}
+
+__device__ __forceinline__ V3 camera_ray(const KParams& p, int px, int py, int sample) {
+    double sx = 0.5, sy = 0.5;
+    if (p.spp > 1) {
+        sx = to_unit(hash_counter(p.seed, (uint64_t)px, (uint64_t)py, 2 * (uint64_t)sample));
+        sy = to_unit(hash_counter(p.seed, (uint64_t)px, (uint64_t)py, 2 * (uint64_t)sample + 1));
+    }
+    const double u = (px + sx) / p.width;
+    const double v = (py + sy) / p.height;
+    const V3 d = add(add(vld(p.forward), scl(vld(p.right), (2.0 * u - 1.0) * p.tan_half_x)),
+                     scl(vld(p.up), (1.0 - 2.0 * v) * p.tan_half_y));
+    return normalized(d);
+}
+
+// ----------------------------------------------------------------- geodesic helpers
+// glibc 2.39 hypot restated (Borges, non-FMA kernel); bit-identical to the
+// reference's std::hypot at geodesic.cpp:78 (verified: tests/test_oracle_geodesic.py).
+__device__ __forceinline__ double hypot_kernel(double ax, double ay) {
+    double t1, t2;
+    double h = sqrt(ax * ax + ay * ay);
+    if (h <= 2.0 * ay) {
+        const double delta = h - ay;
+        t1 = ax * (2.0 * delta - ax);
+        t2 = (delta - 2.0 * (ax - ay)) * delta;
+    } else {
+        const double delta = h - ax;
+        t1 = 2.0 * delta * (ax - 2.0 * ay);
+        t2 = (4.0 * delta - ay) * ay + delta * delta;
+    }
+    h -= (t1 + t2) / (2.0 * h);
+    return h;
+}
+__device__ inline double glibc_hypot(double x, double y) {
+    if (!isfinite(x) || !isfinite(y)) {
+        if (isinf(x) || isinf(y)) return CUDART_INF;
+        return x + y;
+    }
+    x = fabs(x);
+    y = fabs(y);
+    const double ax = x < y ? y : x;
+    const double ay = x < y ? x : y;
+    if (ax > 0x1p+511) {
+        if (ay <= ax * 0x1p-54) return ax + ay;
+        return hypot_kernel(ax * 0x1p-600, ay * 0x1p-600) / 0x1p-600;
+    }
+    if (ay < 0x1p-511) {
+        if (ax >= ay / 0x1p-54) return ax + ay;
+        return hypot_kernel(ax / 0x1p-600, ay / 0x1p-600) * 0x1p-600;
+    }
+    if (ay <= ax * 0x1p-54) return ax + ay;
+    return hypot_kernel(ax, ay);
+}
+
+struct Basis {
+    V3 e1, e2;
+    bool ok;
+};
+
+// geodesic.cpp:49-55
+__device__ __forceinline__ Basis plane_basis(V3 origin, V3 dir, V3 center) {
+    Basis b;
+    b.e1 = normalized(sub(origin, center));
+    const V3 tangential = sub(dir, scl(b.e1, dot(dir, b.e1)));
+    b.ok = !(norm(tangential) < 1e-12);
+    b.e2 = b.ok ? normalized(tangential) : mk(0, 0, 0);
+    return b;
+}
+
+// geodesic.cpp:57-65 (called only with a non-radial ray)
+__device__ __forceinline__ void initial_conditions(V3 origin, V3 dir, V3 center, double& u, double& w) {
+    const V3 v = sub(origin, center);
+    const double r0 = norm(v);
+    const double b = norm(cross(v, dir));
+    u = 1.0 / r0;
+    w = -dot(v, dir) / (r0 * b);
+}
+
+// ----------------------------------------------------------------- record / stats helpers
+__device__ __forceinline__ void warp_add_stats(unsigned long long* stats, unsigned long long steps,
+                                               unsigned long long rej, unsigned long long rays) {
+    for (int o = 16; o > 0; o >>= 1) {
+        steps += __shfl_down_sync(0xffffffffu, steps, o);
+        rej += __shfl_down_sync(0xffffffffu, rej, o);
+        rays += __shfl_down_sync(0xffffffffu, rays, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&stats[0], steps);
+        atomicAdd(&stats[1], rej);
+        atomicAdd(&stats[2], rays);
+    }
+}
+
+struct SampleId {
+    int x, y, s;
+    long long rec;  // record index
+};
+
+__device__ __forceinline__ SampleId sample_of(const KParams& p, long long i) {
+    const long long plane = (long long)p.n_rows * p.width;
+    SampleId id;
+    id.s = (int)(i / plane);
+    const long long pix = i - (long long)id.s * plane;
+    const int j = (int)(pix / p.width);
+    id.x = (int)(pix - (long long)j * p.width);
+    id.y = packed_row_to_y(p, j);
+    id.rec = pix * p.spp + id.s;
+    return id;
+}
+
+// ================================================================= RK4 / RKF45 scene modes
+#define F21 (1.0 / 4.0)
+#define F31 (3.0 / 32.0)
+#define F32 (9.0 / 32.0)
+#define F41 (1932.0 / 2197.0)
+#define F42 (-7200.0 / 2197.0)
+#define F43 (7296.0 / 2197.0)
+#define F51 (439.0 / 216.0)
+#define F52 (-8.0)
+#define F53 (3680.0 / 513.0)
+#define F54 (-845.0 / 4104.0)
+#define F61 (-8.0 / 27.0)
+#define F62 (2.0)
+#define F63 (-3544.0 / 2565.0)
+#define F64 (1859.0 / 4104.0)
+#define F65 (-11.0 / 40.0)
+#define G1 (16.0 / 135.0)
+#define G3 (6656.0 / 12825.0)
+#define G4 (28561.0 / 56430.0)
+#define G5 (-9.0 / 50.0)
+#define G6 (2.0 / 55.0)
+#define H1 (1.0 / 360.0)
+#define H3 (-128.0 / 4275.0)
+#define H4 (-2197.0 / 75240.0)
+#define H5 (1.0 / 50.0)
+#define H6 (2.0 / 55.0)
+
+__device__ __forceinline__ double g_of(double U, double M3) { return U * fma(M3, U, -1.0); }
+
+// One RKF45 step; normative operation order = oracle/bhrt_oracle.c rkf45_step.
+__device__ __forceinline__ bool rkf45_step(double u, double w, double h, double M3, double rtol,
+                                           double atol, double hmax, const double* grow,
+                                           const double* shrink, double& un, double& wn, double& hn) {
+    const double ku1 = w, kw1 = g_of(u, M3);
+    double su, sw;
+    su = F21 * ku1; sw = F21 * kw1;
+    const double U2 = fma(h, su, u), W2 = fma(h, sw, w);
+    const double ku2 = W2, kw2 = g_of(U2, M3);
+    su = F31 * ku1; su = fma(F32, ku2, su);
+    sw = F31 * kw1; sw = fma(F32, kw2, sw);
+    const double U3 = fma(h, su, u), W3 = fma(h, sw, w);
+    const double ku3 = W3, kw3 = g_of(U3, M3);
+    su = F41 * ku1; su = fma(F42, ku2, su); su = fma(F43, ku3, su);
+    sw = F41 * kw1; sw = fma(F42, kw2, sw); sw = fma(F43, kw3, sw);
+    const double U4 = fma(h, su, u), W4 = fma(h, sw, w);
+    const double ku4 = W4, kw4 = g_of(U4, M3);
+    su = F51 * ku1; su = fma(F52, ku2, su); su = fma(F53, ku3, su); su = fma(F54, ku4, su);
+    sw = F51 * kw1; sw = fma(F52, kw2, sw); sw = fma(F53, kw3, sw); sw = fma(F54, kw4, sw);
+    const double U5 = fma(h, su, u), W5 = fma(h, sw, w);
+    const double ku5 = W5, kw5 = g_of(U5, M3);
+    su = F61 * ku1; su = fma(F62, ku2, su); su = fma(F63, ku3, su); su = fma(F64, ku4, su);
+    su = fma(F65, ku5, su);
+    sw = F61 * kw1; sw = fma(F62, kw2, sw); sw = fma(F63, kw3, sw); sw = fma(F64, kw4, sw);
+    sw = fma(F65, kw5, sw);
+    const double U6 = fma(h, su, u), W6 = fma(h, sw, w);
+    const double ku6 = W6, kw6 = g_of(U6, M3);
+    su = G1 * ku1; su = fma(G3, ku3, su); su = fma(G4, ku4, su); su = fma(G5, ku5, su);
+    su = fma(G6, ku6, su);
+    sw = G1 * kw1; sw = fma(G3, kw3, sw); sw = fma(G4, kw4, sw); sw = fma(G5, kw5, sw);
+    sw = fma(G6, kw6, sw);
+    const double u_new = fma(h, su, u), w_new = fma(h, sw, w);
+    su = H1 * ku1; su = fma(H3, ku3, su); su = fma(H4, ku4, su); su = fma(H5, ku5, su);
+    su = fma(H6, ku6, su);
+    sw = H1 * kw1; sw = fma(H3, kw3, sw); sw = fma(H4, kw4, sw); sw = fma(H5, kw5, sw);
+    sw = fma(H6, kw6, sw);
+    const double eu = fabs(h * su), ew = fabs(h * sw);
+    const double du = fma(rtol, fmax(fabs(u), fabs(u_new)), atol);
+    const double dw = fma(rtol, fmax(fabs(w), fabs(w_new)), atol);
+    const bool err_ok = (eu <= du) && (ew <= dw);
+    const bool geo_ok = u_new >= 0.5 * u;
+    const int du_ = __double2hiint(eu) - __double2hiint(du);
+    const int dw_ = __double2hiint(ew) - __double2hiint(dw);
+    int q = (du_ > dw_ ? du_ : dw_) >> 18;
+    q = q < kQMin ? kQMin : (q > kQMin + kQN - 1 ? kQMin + kQN - 1 : q);
+    if (err_ok && geo_ok) {
+        un = u_new;
+        wn = w_new;
+        hn = fmin(h * grow[q - kQMin], hmax);
+        return true;
+    }
+    hn = err_ok ? 0.5 * h : h * shrink[q - kQMin];
+    return false;
+}
+
+// tests/oracles.hpp:23-30 (reference arithmetic, no FMA)
+__device__ __forceinline__ void rk4_step(double u, double w, double h, double mass, double& un,
+                                         double& wn) {
+    const double k1u = w, k1w = 3.0 * mass * u * u - u;
+    const double a2 = u + 0.5 * h * k1u, b2 = w + 0.5 * h * k1w;
+    const double k2u = b2, k2w = 3.0 * mass * a2 * a2 - a2;
+    const double a3 = u + 0.5 * h * k2u, b3 = w + 0.5 * h * k2w;
+    const double k3u = b3, k3w = 3.0 * mass * a3 * a3 - a3;
+    const double a4 = u + h * k3u, b4 = w + h * k3w;
+    const double k4u = b4, k4w = 3.0 * mass * a4 * a4 - a4;
+    un = u + h / 6.0 * (k1u + 2.0 * k2u + 2.0 * k3u + k4u);
+    wn = w + h / 6.0 * (k1w + 2.0 * k2w + 2.0 * k3w + k4w);
+}
+
+// Cubic Hermite interpolant of u over one step in monomial form (oracle
+// hermite_coef / hermite_eval / hermite_deval, same op order).
+struct Cubic {
+    double a0, a1, a2, a3;
+};
+__device__ __forceinline__ Cubic hermite_coef(double h, double ua, double wa, double ub, double wb) {
+    Cubic c;
+    c.a0 = ua;
+    c.a1 = h * wa;
+    c.a2 = 3.0 * (ub - ua) - h * (2.0 * wa + wb);
+    c.a3 = 2.0 * (ua - ub) + h * (wa + wb);
+    return c;
+}
+__device__ __forceinline__ double hermite_eval(const Cubic& c, double t) {
+    return fma(fma(fma(c.a3, t, c.a2), t, c.a1), t, c.a0);
+}
+__device__ __forceinline__ double hermite_deval(const Cubic& c, double t) {
+    return fma(fma(3.0 * c.a3, t, 2.0 * c.a2), t, c.a1);
+}
+
+}  // namespace bhrt_b200

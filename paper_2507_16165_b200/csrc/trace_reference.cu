@@ -1,0 +1,191 @@
+// trace_reference.cu — mode R: the reference algorithm on the GPU.
+//
+// DOPRI5(4)+PI control inside epsilon-windows, window-end termination tests
+// and last-chord escape direction, exactly as geodesic.cpp:84-238, one
+// sample per thread. Compiled with --fmad=false (like the reference's x86-64
+// build) and glibc's hypot restated, so window states are bit-identical to
+// the reference; only pow() (step-hint only) and sin/cos (last chord) may
+// differ by ulps (libdevice vs glibc).
+#include "device_common.cuh"
+
+namespace bhrt_b200 {
+
+// ================================================================= mode R
+// Dormand-Prince 5(4) tableau (geodesic.cpp:89-100), same constant expressions.
+#define A21 (1.0 / 5.0)
+#define A31 (3.0 / 40.0)
+#define A32 (9.0 / 40.0)
+#define A41 (44.0 / 45.0)
+#define A42 (-56.0 / 15.0)
+#define A43 (32.0 / 9.0)
+#define A51 (19372.0 / 6561.0)
+#define A52 (-25360.0 / 2187.0)
+#define A53 (64448.0 / 6561.0)
+#define A54 (-212.0 / 729.0)
+#define A61 (9017.0 / 3168.0)
+#define A62 (-355.0 / 33.0)
+#define A63 (46732.0 / 5247.0)
+#define A64 (49.0 / 176.0)
+#define A65 (-5103.0 / 18656.0)
+#define B1 (35.0 / 384.0)
+#define B3 (500.0 / 1113.0)
+#define B4 (125.0 / 192.0)
+#define B5 (-2187.0 / 6784.0)
+#define B6 (11.0 / 84.0)
+#define E1 (71.0 / 57600.0)
+#define E3 (-71.0 / 16695.0)
+#define E4 (71.0 / 1920.0)
+#define E5 (-17253.0 / 339200.0)
+#define E6 (22.0 / 525.0)
+#define E7 (-1.0 / 40.0)
+
+__device__ __forceinline__ double rhs_w(double u, double mass) { return 3.0 * mass * u * u - u; }
+
+// geodesic.cpp:84-162. Returns false on StepSizeUnderflow (phi/u/w then hold
+// the failure state, as StepSizeUnderflow::state does).
+__device__ bool integrate_window(double& phi, double& u, double& w, double dphi, double mass,
+                                 double rtol, double atol, double& hint, unsigned& nsteps,
+                                 unsigned& nrej) {
+    double y0 = u, y1 = w;
+    double k10 = y1, k11 = rhs_w(y0, mass);
+    double remaining = dphi;
+    double h = hint > 0.0 ? dmin(hint, dphi) : dphi;
+    double err_prev = 1e-4;
+    while (remaining > 0.0) {
+        const double h_try = dmin(h, remaining);
+        double t0, t1;
+        t0 = y0 + h_try * A21 * k10;
+        t1 = y1 + h_try * A21 * k11;
+        const double k20 = t1, k21 = rhs_w(t0, mass);
+        t0 = y0 + h_try * (A31 * k10 + A32 * k20);
+        t1 = y1 + h_try * (A31 * k11 + A32 * k21);
+        const double k30 = t1, k31 = rhs_w(t0, mass);
+        t0 = y0 + h_try * (A41 * k10 + A42 * k20 + A43 * k30);
+        t1 = y1 + h_try * (A41 * k11 + A42 * k21 + A43 * k31);
+        const double k40 = t1, k41 = rhs_w(t0, mass);
+        t0 = y0 + h_try * (A51 * k10 + A52 * k20 + A53 * k30 + A54 * k40);
+        t1 = y1 + h_try * (A51 * k11 + A52 * k21 + A53 * k31 + A54 * k41);
+        const double k50 = t1, k51 = rhs_w(t0, mass);
+        t0 = y0 + h_try * (A61 * k10 + A62 * k20 + A63 * k30 + A64 * k40 + A65 * k50);
+        t1 = y1 + h_try * (A61 * k11 + A62 * k21 + A63 * k31 + A64 * k41 + A65 * k51);
+        const double k60 = t1, k61 = rhs_w(t0, mass);
+        const double n0 = y0 + h_try * (B1 * k10 + B3 * k30 + B4 * k40 + B5 * k50 + B6 * k60);
+        const double n1 = y1 + h_try * (B1 * k11 + B3 * k31 + B4 * k41 + B5 * k51 + B6 * k61);
+        const double k70 = n1, k71 = rhs_w(n0, mass);
+        const double e0 = h_try * (E1 * k10 + E3 * k30 + E4 * k40 + E5 * k50 + E6 * k60 + E7 * k70);
+        const double e1 = h_try * (E1 * k11 + E3 * k31 + E4 * k41 + E5 * k51 + E6 * k61 + E7 * k71);
+        const double s0 = atol + rtol * dmax(fabs(y0), fabs(n0));
+        const double s1 = atol + rtol * dmax(fabs(y1), fabs(n1));
+        double err = 0.0;
+        err += (e0 / s0) * (e0 / s0);
+        err += (e1 / s1) * (e1 / s1);
+        err = sqrt(err / 2.0);
+        if (err <= 1.0) {
+            y0 = n0;
+            y1 = n1;
+            k10 = k70;
+            k11 = k71;
+            remaining -= h_try;
+            const double factor =
+                clampd(0.9 * pow(err, -0.7 / 5.0) * pow(err_prev, 0.4 / 5.0), 0.2, 5.0);
+            h = h_try * factor;
+            err_prev = dmax(err, 1e-4);
+            ++nsteps;
+        } else {
+            h = h_try * clampd(0.9 * pow(err, -0.2), 0.1, 0.9);
+            ++nrej;
+        }
+        if (h < 1e-14 && remaining > 0.0) {
+            phi = phi + (dphi - remaining);
+            u = y0;
+            w = y1;
+            return false;
+        }
+    }
+    hint = h;
+    phi = phi + dphi;
+    u = y0;
+    w = y1;
+    return true;
+}
+
+// OrbitalPlaneBasis::point (geodesic.cpp:37-39)
+__device__ __forceinline__ V3 plane_point(V3 origin, V3 e1, V3 e2, double r, double phi) {
+    return add(origin, scl(add(scl(e1, cos(phi)), scl(e2, sin(phi))), r));
+}
+
+__global__ void __launch_bounds__(128) trace_reference_kernel(const __grid_constant__ KParams p) {
+    const long long n = (long long)p.n_rows * p.width * p.spp;
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned nsteps = 0, nrej = 0;
+    if (i < n) {
+        const SampleId id = sample_of(p, i);
+        bhrt_ray_record rec;
+        rec.sphere = -1;
+        rec.point[0] = rec.point[1] = rec.point[2] = 0.0;
+        rec.phi = 0.0;
+        const V3 origin = vld(p.cam_pos), center = vld(p.center);
+        const V3 dir = camera_ray(p, id.x, id.y, id.s);
+        const V3 v = sub(origin, center);
+        const double r0 = norm(v);
+        const Basis B = plane_basis(origin, dir, center);
+        int obj;
+        V3 edir = dir;
+        if (!B.ok) {  // radial: geodesic.cpp:175-187
+            obj = dot(dir, sub(center, origin)) > 0.0 ? BHRT_OBJ_HORIZON : BHRT_OBJ_SKY;
+            (void)r0;
+        } else {
+            double u, w, phi = 0.0, hint = 0.0;
+            initial_conditions(origin, dir, center, u, w);
+            double prev_phi = 0.0, prev_u = 0.0, last_phi = 0.0, last_u = 0.0;
+            int npts = 1;
+            obj = BHRT_OBJ_NONE;
+            for (;;) {
+                if (u >= p.u_cap) { obj = BHRT_OBJ_HORIZON; break; }
+                if (u <= p.u_esc && w < 0.0) {
+                    obj = BHRT_OBJ_SKY;
+                    if (npts >= 2) {
+                        const V3 last = plane_point(center, B.e1, B.e2, 1.0 / last_u, last_phi);
+                        const V3 prev = npts == 2 ? origin
+                                                  : plane_point(center, B.e1, B.e2, 1.0 / prev_u, prev_phi);
+                        edir = normalized(sub(last, prev));
+                    }
+                    break;
+                }
+                if (phi > p.phi_max) { obj = BHRT_OBJ_STALLED; break; }
+                // segment_dphi, geodesic.cpp:76-80
+                const double hyp = glibc_hypot(u, w);
+                const double dphi = clampd(p.epsilon * u * u / hyp, 1e-6, 0.1);
+                if (!integrate_window(phi, u, w, dphi, p.mass, p.rel_tol, p.abs_tol, hint, nsteps, nrej)) {
+                    if (p.mass > 0.0 && u >= p.u_cap) { obj = BHRT_OBJ_HORIZON; break; }
+                    obj = -BHRT_NUMERICAL;
+                    break;
+                }
+                if (!(u > 0.0)) { obj = -BHRT_NUMERICAL; break; }
+                prev_phi = last_phi;
+                prev_u = last_u;
+                last_phi = phi;
+                last_u = u;
+                ++npts;
+            }
+            rec.phi = phi;
+        }
+        rec.object = obj;
+        if (obj == BHRT_OBJ_SKY) {
+            rec.point[0] = edir.x;
+            rec.point[1] = edir.y;
+            rec.point[2] = edir.z;
+        }
+        rec.steps = (int)nsteps;
+        rec.rejected = (int)nrej;
+        p.records[id.rec] = rec;
+    }
+    warp_add_stats(p.stats, nsteps, nrej, i < n ? 1ull : 0ull);
+}
+
+void launch_reference(const KParams& p, cudaStream_t st) {
+    const long long n = (long long)p.n_rows * p.width * p.spp;
+    trace_reference_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(p);
+}
+
+}  // namespace bhrt_b200

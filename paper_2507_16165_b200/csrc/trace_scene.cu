@@ -1,0 +1,486 @@
+// trace_scene.cu — RK4 / RKF45 renderers with disk + sphere hit tests.
+//
+// One sample per thread. The hot loop keeps only (phi, u, w, h), the state
+// before the last step and the next event angle in registers; the ray's
+// orbital-plane frame, disk line and sphere-candidate windows live in
+// per-thread shared-memory slots (lane-major, conflict-free) that only setup,
+// event steps and escape touch. Operation order mirrors the oracle
+// (oracle/bhrt_oracle.c trace_scene / step_events / escape_dir), so records
+// are bit-identical up to libdevice transcendentals outside the step.
+#include "device_common.cuh"
+
+namespace bhrt_b200 {
+
+constexpr int kBlock = 128;
+constexpr int kSlots = 8;
+constexpr int kSphSm = 128;          // spheres staged in shared memory
+constexpr float kWinMargin = 5e-4f;  // fp32 window slack (rad); windows only cull
+#ifndef BHRT_SCENE_MINB
+#define BHRT_SCENE_MINB 5  // min resident blocks per SM (register cap), tuned on B200
+#endif
+
+struct SceneSm {
+    float4 sph[kSphSm];  // (cx, cy, cz, r + fp32 slack) relative to the hole: cull prefilter
+    double grow[kQN], shrink[kQN];
+    double e1[3][kBlock], e2[3][kBlock], n[3][kBlock];
+    double dl[2][kBlock];  // unit disk line, orbital-plane coordinates
+    double dL[2][kBlock];  // unit disk line, world x and z (y = 0)
+    double sigma[kBlock], energy[kBlock], next_disk[kBlock];
+    float lo[kSlots][kBlock], hi[kSlots][kBlock];
+    unsigned char k[kSlots][kBlock];
+    int nc[kBlock];
+    float next_sph[kBlock];
+};
+
+__device__ __forceinline__ V3 ld3(const double (&a)[3][kBlock], int t) { return {a[0][t], a[1][t], a[2][t]}; }
+__device__ __forceinline__ void st3(double (&a)[3][kBlock], int t, V3 v) {
+    a[0][t] = v.x;
+    a[1][t] = v.y;
+    a[2][t] = v.z;
+}
+
+// Sphere centre relative to the hole, in the oracle's order (center - O).
+__device__ __forceinline__ V3 sphere_c(const KParams& p, int k) {
+    const bhrt_sphere& s = p.spheres[k];
+    return {__ldg(&s.center[0]) - p.center[0], __ldg(&s.center[1]) - p.center[1],
+            __ldg(&s.center[2]) - p.center[2]};
+}
+
+__device__ __forceinline__ void sphere_window_f(double cx, double cy, double rho2, float& lo, float& hi) {
+    const double q = cx * cx + cy * cy - rho2;  // rc^2 - rho^2
+    if (!(q > 0.0)) {
+        lo = -CUDART_INF_F;
+        hi = CUDART_INF_F;
+        return;
+    }
+    const float a = atan2f((float)sqrt(rho2), (float)sqrt(q));  // asin(rho / rc)
+    const float pc = atan2f((float)cy, (float)cx);
+    lo = pc - a - kWinMargin;
+    hi = pc + a + kWinMargin;
+    if (hi < 0.0f) {
+        lo += 2.0f * (float)PI_D;
+        hi += 2.0f * (float)PI_D;
+    }
+}
+
+// Disk line + sphere candidates (oracle ray_events_setup). Returns the first
+// event angle.
+__device__ double events_setup(const KParams& p, SceneSm& sm, int t, V3 e1, V3 e2, V3 n) {
+    double next_disk = CUDART_INF;
+    sm.sigma[t] = 1.0;
+    if (p.disk_enabled) {
+        const V3 L = mk(-n.z, 0.0, n.x);
+        const double nl = norm(L);
+        if (nl >= 1e-12) {
+            const double lx = dot(L, e1), ly = dot(L, e2);
+            const double pl = atan2(ly, lx);
+            next_disk = pl > 0.0 ? pl : pl + PI_D;
+            sm.sigma[t] = pl > 0.0 ? 1.0 : -1.0;
+            sm.dl[0][t] = lx / nl;
+            sm.dl[1][t] = ly / nl;
+            sm.dL[0][t] = L.x / nl;
+            sm.dL[1][t] = L.z / nl;
+        }
+    }
+    sm.next_disk[t] = next_disk;
+    int nc = 0;
+    float next_sph = CUDART_INF_F;
+    const float nxf = (float)n.x, nyf = (float)n.y, nzf = (float)n.z;
+    const int ns = p.n_spheres;
+    for (int k = 0; k < ns; ++k) {
+        bool maybe = true;
+        if (k < kSphSm) {  // conservative fp32 prefilter; the fp64 test below decides
+            const float4 f = sm.sph[k];
+            const float dnf = f.x * nxf + f.y * nyf + f.z * nzf;
+            maybe = fabsf(dnf) < f.w;
+        }
+        if (!maybe) continue;
+        const V3 c = sphere_c(p, k);
+        const double r = __ldg(&p.spheres[k].radius);
+        const double dn = dot(c, n);
+        if (!(fabs(dn) < r)) continue;
+        if (nc == kSlots) {
+            nc = -1;
+            break;
+        }
+        const double cx = dot(c, e1), cy = dot(c, e2);
+        const double rho2 = r * r - dn * dn;
+        float lo, hi;
+        sphere_window_f(cx, cy, rho2, lo, hi);
+        sm.lo[nc][t] = lo;
+        sm.hi[nc][t] = hi;
+        sm.k[nc][t] = (unsigned char)k;
+        next_sph = fminf(next_sph, lo);
+        ++nc;
+    }
+    if (nc < 0) next_sph = -CUDART_INF_F;
+    sm.nc[t] = nc;
+    sm.next_sph[t] = next_sph;
+    return dmin(next_disk, (double)next_sph);
+}
+
+struct Hit {
+    int obj, sphere;
+    V3 point;
+};
+
+// Oracle step_events(): disk = exact phi-event on the step's Hermite
+// interpolant; spheres = first entering hit on S equal-angle sub-chords.
+// Returns true on hit; always advances the event state and next_ev.
+__device__ __noinline__ bool step_events(const KParams& p, SceneSm& sm, int t, double pa, double ua,
+                                         double wa, double pb, double ub, double wb, double& next_ev,
+                                         Hit& hit) {
+    const double h = pb - pa;
+    const Cubic cu = hermite_coef(h, ua, wa, ub, wb);
+    double next_disk = sm.next_disk[t];
+    // ---- disk
+    bool disk_hit = false;
+    double r_ev = 0.0, dlx = 0.0, dly = 0.0;
+    const double sigma = sm.sigma[t];
+    if (next_disk > pa && next_disk <= pb) {
+        const double tt = (next_disk - pa) / h;
+        const double u_ev = hermite_eval(cu, tt);
+        if (u_ev > 0.0) {
+            r_ev = 1.0 / u_ev;
+            if (r_ev >= p.disk_r_in && r_ev <= p.disk_r_out) {
+                disk_hit = true;
+                dlx = sigma * sm.dl[0][t];
+                dly = sigma * sm.dl[1][t];
+            }
+        }
+    }
+    // ---- spheres
+    const int nc = sm.nc[t];
+    const bool test_all = nc < 0;
+    unsigned act = 0;
+    if (!test_all) {
+        const float fa = (float)pa, fb = (float)pb;
+        for (int i = 0; i < nc; ++i)
+            if (sm.lo[i][t] <= fb && sm.hi[i][t] >= fa) act |= 1u << i;
+    }
+    bool sph_hit = false;
+    int bsph = -1;
+    double bqx = 0.0, bqy = 0.0;
+    if (act || test_all) {
+        // Candidate-outer evaluation of the oracle's sub-chord-outer search:
+        // each candidate scans only the sub-chords its (conservative) window
+        // overlaps and stops at its first hit; the winner is the
+        // lexicographic minimum of (sub-chord, chord parameter), ties to the
+        // lower slot — the same hit the oracle finds.
+        const V3 e1 = ld3(sm.e1, t), e2 = ld3(sm.e2, t), n = ld3(sm.n, t);
+        int S = 1;
+        if (h > p.chord_dphi) S = (int)ceil(h / p.chord_dphi);
+        const double dl = h / S;
+        const double cd_ = cos(dl), sd_ = sin(dl);
+        const double c0 = cos(pa), s0 = sin(pa);
+        const float fpa = (float)pa, fdl = (float)dl;
+        int best_j = S;
+        double best_t = CUDART_INF;
+        const int ncand = test_all ? p.n_spheres : nc;
+        for (int a = 0; a < ncand; ++a) {
+            int k, j0 = 0, j1 = S - 1;
+            if (test_all) {
+                k = a;
+            } else {
+                if (!(act & (1u << a))) continue;
+                k = sm.k[a][t];
+                // clamp in float first: windows may be infinite
+                const float fS = (float)S;
+                j0 = (int)fminf(fmaxf(floorf((sm.lo[a][t] - fpa) / fdl) - 1.0f, 0.0f), fS);
+                j1 = (int)fminf(fmaxf(floorf((sm.hi[a][t] - fpa) / fdl) + 1.0f, 0.0f), fS - 1.0f);
+            }
+            j1 = min(j1, best_j);
+            if (j0 > j1) continue;
+            const V3 c = sphere_c(p, k);
+            const double r = __ldg(&p.spheres[k].radius);
+            const double dn = dot(c, n);
+            if (!(fabs(dn) < r)) continue;
+            const double ccx = dot(c, e1), ccy = dot(c, e2);
+            const double rho2 = r * r - dn * dn;
+            double cj = c0, sj = s0;
+            for (int j = 0; j < j0; ++j) {  // same recurrence values as the sequential walk
+                const double ck = cj * cd_ - sj * sd_;
+                sj = sj * cd_ + cj * sd_;
+                cj = ck;
+            }
+            const double uj = j0 == 0 ? ua : hermite_eval(cu, (double)j0 / S);
+            const double rj = 1.0 / uj;
+            double xj = cj * rj, yj = sj * rj;
+            for (int j = j0; j <= j1; ++j) {
+                const double ck = cj * cd_ - sj * sd_;
+                const double sk = sj * cd_ + cj * sd_;
+                const double uk = (j + 1 == S) ? ub : hermite_eval(cu, (double)(j + 1) / S);
+                const double rk = 1.0 / uk;
+                const double xk = ck * rk, yk = sk * rk;
+                const double dx = xk - xj, dy = yk - yj;
+                const double mx = xj - ccx, my = yj - ccy;
+                const double A = dx * dx + dy * dy;
+                const double Bq = mx * dx + my * dy;
+                const double Cq = mx * mx + my * my - rho2;
+                if (Cq > 0.0) {
+                    const double disc = Bq * Bq - A * Cq;
+                    if (!(disc < 0.0)) {
+                        const double tq = (-Bq - sqrt(disc)) / A;
+                        if (tq >= 0.0 && tq <= 1.0) {
+                            if (j < best_j || tq < best_t) {
+                                best_j = j;
+                                best_t = tq;
+                                bsph = k;
+                                bqx = xj + tq * dx;
+                                bqy = yj + tq * dy;
+                            }
+                            break;
+                        }
+                    }
+                }
+                cj = ck;
+                sj = sk;
+                xj = xk;
+                yj = yk;
+            }
+        }
+        sph_hit = best_j < S;
+        if (sph_hit) {
+            hit.point = add(vld(p.center), add(scl(e1, bqx), scl(e2, bqy)));
+        }
+    }
+    if (sph_hit && disk_hit) {
+        if (bqx * dly - bqy * dlx > 0.0)
+            disk_hit = false;
+        else
+            sph_hit = false;
+    }
+    if (disk_hit) {
+        hit.obj = BHRT_OBJ_DISK;
+        hit.sphere = -1;
+        const V3 Lw = mk(sm.dL[0][t], 0.0, sm.dL[1][t]);
+        hit.point = add(vld(p.center), scl(Lw, sigma * r_ev));
+    } else if (sph_hit) {
+        hit.obj = BHRT_OBJ_SPHERE;
+        hit.sphere = bsph;
+    }
+    // advance the event state past pb
+    if (next_disk <= pb) {
+        double sg = sigma;
+        while (next_disk <= pb) {
+            next_disk += PI_D;
+            sg = -sg;
+        }
+        sm.next_disk[t] = next_disk;
+        sm.sigma[t] = sg;
+    }
+    float next_sph = sm.next_sph[t];
+    if (!test_all) {
+        next_sph = CUDART_INF_F;
+        const float fb = (float)pb;
+        for (int i = 0; i < nc; ++i) {
+            float lo = sm.lo[i][t], hi = sm.hi[i][t];
+            if (hi < fb) {
+                while (hi < fb) {
+                    lo += 2.0f * (float)PI_D;
+                    hi += 2.0f * (float)PI_D;
+                }
+                sm.lo[i][t] = lo;
+                sm.hi[i][t] = hi;
+            }
+            next_sph = fminf(next_sph, lo);
+        }
+        sm.next_sph[t] = next_sph;
+    }
+    next_ev = dmin(next_disk, (double)next_sph);
+    return disk_hit || sph_hit;
+}
+
+__device__ __forceinline__ V3 tangent_dir(V3 e1, V3 e2, double phi, double u, double w) {
+    const double c = cos(phi), sn = sin(phi);
+    const double tx = -u * sn - w * c, ty = u * c - w * sn;
+    return normalized(add(scl(e1, tx), scl(e2, ty)));
+}
+
+// Oracle escape_dir(): tangent at the r = escape_radius crossing of the last
+// step (Hermite + 2 Newton iterations, u' from the first integral).
+__device__ __noinline__ V3 escape_dir(const KParams& p, SceneSm& sm, int t, bool has_step, double pa,
+                                      double ua, double wa, double pb, double ub, double wb) {
+    const V3 e1 = ld3(sm.e1, t), e2 = ld3(sm.e2, t);
+    if (!has_step || !(ua > p.u_esc)) return tangent_dir(e1, e2, pb, ub, wb);
+    const double u_esc = p.u_esc;
+    const double h = pb - pa;
+    const Cubic cu = hermite_coef(h, ua, wa, ub, wb);
+    double tt = (ua - u_esc) / (ua - ub);
+    for (int it = 0; it < 2; ++it) {
+        const double f = hermite_eval(cu, tt) - u_esc;
+        const double df = hermite_deval(cu, tt);
+        if (df != 0.0) tt = tt - f / df;
+        tt = clampd(tt, 0.0, 1.0);
+    }
+    const double us = hermite_eval(cu, tt);
+    const double M2 = 2.0 * p.mass;
+    const double q = sm.energy[t] - us * us + M2 * us * us * us;
+    const double ws = -sqrt(q > 0.0 ? q : 0.0);
+    return tangent_dir(e1, e2, pa + h * tt, us, ws);
+}
+
+// Straight radial ray (geodesic.cpp:175-187) with scene hit tests.
+__device__ __noinline__ Hit radial_scene(const KParams& p, V3 origin, V3 dir, double seg_len, bool captured) {
+    const V3 O = vld(p.center);
+    double best = seg_len;
+    Hit H;
+    H.obj = captured ? BHRT_OBJ_HORIZON : BHRT_OBJ_SKY;
+    H.sphere = -1;
+    if (p.disk_enabled && dir.y != 0.0) {
+        const double tq = (O.y - origin.y) / dir.y;
+        if (tq >= 0.0 && tq <= best) {
+            const V3 q = sub(add(origin, scl(dir, tq)), O);
+            const double rq = sqrt(q.x * q.x + q.z * q.z);
+            if (rq >= p.disk_r_in && rq <= p.disk_r_out) {
+                best = tq;
+                H.obj = BHRT_OBJ_DISK;
+            }
+        }
+    }
+    for (int k = 0; k < p.n_spheres; ++k) {
+        const bhrt_sphere& sp = p.spheres[k];
+        const V3 m = sub(origin, vld(sp.center));
+        const double B = dot(m, dir), Cq = dot(m, m) - sp.radius * sp.radius;
+        if (!(Cq > 0.0)) continue;
+        const double disc = B * B - Cq;
+        if (disc < 0.0) continue;
+        const double tq = -B - sqrt(disc);
+        if (tq >= 0.0 && tq < best) {
+            best = tq;
+            H.obj = BHRT_OBJ_SPHERE;
+            H.sphere = k;
+        }
+    }
+    H.point = H.obj == BHRT_OBJ_SKY ? dir : add(origin, scl(dir, best));
+    return H;
+}
+
+template <int INTEG>
+__global__ void __launch_bounds__(kBlock, BHRT_SCENE_MINB) trace_scene_kernel(const __grid_constant__ KParams p) {
+    __shared__ SceneSm sm;
+    const int t = threadIdx.x;
+    for (int k = t; k < p.n_spheres && k < kSphSm; k += blockDim.x) {
+        const V3 c = sphere_c(p, k);
+        const double r = p.spheres[k].radius;
+        const float slack = 1e-5f * (float)(norm(c) + r) + 1e-6f;
+        sm.sph[k] = make_float4((float)c.x, (float)c.y, (float)c.z, (float)r + slack);
+    }
+    if (INTEG == BHRT_INTEGRATOR_RKF45)
+        for (int k = t; k < kQN; k += blockDim.x) {
+            sm.grow[k] = p.grow[k];
+            sm.shrink[k] = p.shrink[k];
+        }
+    __syncthreads();
+
+    const long long n = (long long)p.n_rows * p.width * p.spp;
+    const long long i = (long long)blockIdx.x * blockDim.x + t;
+    unsigned nsteps = 0, nrej = 0;
+    if (i < n) {
+        const SampleId id = sample_of(p, i);
+        const V3 origin = vld(p.cam_pos), O = vld(p.center);
+        const V3 dir = camera_ray(p, id.x, id.y, id.s);
+        const Basis B = plane_basis(origin, dir, O);
+        Hit H;
+        H.obj = BHRT_OBJ_NONE;
+        H.sphere = -1;
+        H.point = mk(0.0, 0.0, 0.0);
+        double phi = 0.0;
+        if (!B.ok) {
+            const double r0 = norm(sub(origin, O));
+            const bool cap = dot(dir, sub(O, origin)) > 0.0;
+            H = radial_scene(p, origin, dir, cap ? r0 - 2.0 * p.mass : p.escape_radius, cap);
+        } else {
+            const V3 nrm = cross(B.e1, B.e2);
+            st3(sm.e1, t, B.e1);
+            st3(sm.e2, t, B.e2);
+            st3(sm.n, t, nrm);
+            double u, w;
+            initial_conditions(origin, dir, O, u, w);
+            sm.energy[t] = w * w + u * u - (2.0 * p.mass) * u * u * u;
+            double next_ev = events_setup(p, sm, t, B.e1, B.e2, nrm);
+            double pp = 0.0, up = 0.0, wp = 0.0;  // state before the last accepted step
+            bool has_step = false;
+            if (INTEG == BHRT_INTEGRATOR_RK4) {
+                const double h = p.step;
+                for (;;) {  // tests/oracles.hpp:47-54 loop structure
+                    if (!(phi < p.phi_max)) { H.obj = BHRT_OBJ_STALLED; break; }
+                    if (u >= p.u_cap) { H.obj = BHRT_OBJ_HORIZON; break; }
+                    if (u <= p.u_esc && w < 0.0) { H.obj = BHRT_OBJ_SKY; break; }
+                    double un, wn;
+                    rk4_step(u, w, h, p.mass, un, wn);
+                    const double pn = phi + h;
+                    ++nsteps;
+                    if (pn >= next_ev && step_events(p, sm, t, phi, u, w, pn, un, wn, next_ev, H)) {
+                        phi = pn;
+                        break;
+                    }
+                    pp = phi;
+                    up = u;
+                    wp = w;
+                    has_step = true;
+                    phi = pn;
+                    u = un;
+                    w = wn;
+                    if (!(u > 0.0)) { H.obj = -BHRT_NUMERICAL; break; }
+                }
+            } else {
+                double h = p.step;
+                for (;;) {  // geodesic.cpp:199-236 loop structure
+                    if (u >= p.u_cap) { H.obj = BHRT_OBJ_HORIZON; break; }
+                    if (u <= p.u_esc && w < 0.0) { H.obj = BHRT_OBJ_SKY; break; }
+                    if (phi > p.phi_max) { H.obj = BHRT_OBJ_STALLED; break; }
+                    double un, wn, hn;
+                    if (rkf45_step(u, w, h, p.M3, p.rel_tol, p.abs_tol, p.max_step, sm.grow, sm.shrink, un,
+                                   wn, hn)) {
+                        const double pn = phi + h;
+                        ++nsteps;
+                        if (pn >= next_ev && step_events(p, sm, t, phi, u, w, pn, un, wn, next_ev, H)) {
+                            phi = pn;
+                            break;
+                        }
+                        pp = phi;
+                        up = u;
+                        wp = w;
+                        has_step = true;
+                        phi = pn;
+                        u = un;
+                        w = wn;
+                        if (!(u > 0.0)) { H.obj = -BHRT_NUMERICAL; break; }
+                    } else {
+                        ++nrej;
+                    }
+                    h = hn;
+                    if (h < 1e-14) {
+                        H.obj = (p.mass > 0.0 && u >= p.u_cap) ? BHRT_OBJ_HORIZON : -BHRT_NUMERICAL;
+                        break;
+                    }
+                }
+            }
+            if (H.obj == BHRT_OBJ_SKY) H.point = escape_dir(p, sm, t, has_step, pp, up, wp, phi, u, w);
+        }
+        bhrt_ray_record rec;
+        rec.object = H.obj;
+        rec.sphere = H.sphere;
+        const bool has_point = H.obj == BHRT_OBJ_SKY || H.obj == BHRT_OBJ_DISK || H.obj == BHRT_OBJ_SPHERE;
+        rec.point[0] = has_point ? H.point.x : 0.0;
+        rec.point[1] = has_point ? H.point.y : 0.0;
+        rec.point[2] = has_point ? H.point.z : 0.0;
+        rec.phi = phi;
+        rec.steps = (int)nsteps;
+        rec.rejected = (int)nrej;
+        p.records[id.rec] = rec;
+    }
+    warp_add_stats(p.stats, nsteps, nrej, i < n ? 1ull : 0ull);
+}
+
+void launch_scene(const KParams& p, cudaStream_t st) {
+    const long long n = (long long)p.n_rows * p.width * p.spp;
+    const unsigned blocks = (unsigned)((n + kBlock - 1) / kBlock);
+    if (p.integrator == BHRT_INTEGRATOR_RK4)
+        trace_scene_kernel<BHRT_INTEGRATOR_RK4><<<blocks, kBlock, 0, st>>>(p);
+    else
+        trace_scene_kernel<BHRT_INTEGRATOR_RKF45><<<blocks, kBlock, 0, st>>>(p);
+}
+
+}  // namespace bhrt_b200

@@ -11,7 +11,8 @@ import os
 from .abi import RayRecord, Scene, Sphere, StatusInfo
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libbhrt_b200.so")
+# BHRT_B200_LIB: developer override to time alternative builds of the same sources
+LIB_PATH = os.environ.get("BHRT_B200_LIB") or os.path.join(_PKG, "libbhrt_b200.so")
 
 _lib = None
 
