@@ -60,6 +60,44 @@ def build(verbose: bool = False, force: bool = False) -> str:
     return LIB
 
 
+REF = "/root/reference/proj"
+DROPIN = os.path.join(PKG, "dropin")
+
+
+def build_dropin(force: bool = False) -> bool:
+    """Drop-in artefacts that compile against the reference's own headers
+    and non-hot-path sources (only where /root/reference exists; the built
+    files travel to the GPU box like the .so):
+
+      dropin/libbhrt_render_b200.so   render.hpp surface over the C ABI
+      dropin/bhrt_worker_b200         `bhrt worker` (BHRT protocol) on the GPU
+      dropin/acceptance_b200          the reference's acceptance suite, its
+                                      render.cpp replaced by render_shim.cpp
+    """
+    if not os.path.isdir(os.path.join(REF, "src")):
+        return False
+    os.makedirs(DROPIN, exist_ok=True)
+    shim = os.path.join(CSRC, "render_shim.cpp")
+    worker = os.path.join(CSRC, "worker_main.cpp")
+    outs = [os.path.join(DROPIN, n) for n in
+            ("libbhrt_render_b200.so", "bhrt_worker_b200", "acceptance_b200")]
+    deps = [shim, worker, LIB, os.path.join(ROOT, "include", "bhrt_cuda.h")]
+    if not force and all(not _stale(o, deps) for o in outs):
+        return True
+    cxx = ["g++", "-std=c++20", "-O2", "-fPIC", "-include", "algorithm", "-I" + os.path.join(REF, "include"),
+           "-I" + os.path.join(ROOT, "include")]
+    # the reference's sources minus render.cpp (the replaced hot path)
+    srcs = [os.path.join(REF, "src", f) for f in sorted(os.listdir(os.path.join(REF, "src")))
+            if f.endswith(".cpp") and f != "render.cpp"]
+    link = ["-L" + PKG, "-lbhrt_b200", "-Wl,-rpath," + PKG, "-Wl,-rpath,$ORIGIN/..", "-lpthread"]
+    subprocess.run([*cxx, "-shared", "-o", outs[0], shim, *link], check=True)
+    subprocess.run([*cxx, "-o", outs[1], worker, shim, *srcs, *link], check=True)
+    subprocess.run([*cxx, f'-DBHRT_BINARY="{os.path.join("/root/repo", os.path.relpath(outs[1], ROOT))}"',
+                    "-o", outs[2], os.path.join(REF, "tests", "acceptance.cpp"), shim, *srcs, *link],
+                   check=True)
+    return True
+
+
 def build_oracle() -> None:
     """The CPU checker (oracle/liboracle.so) and, where /root/reference exists,
     the compiled reference (oracle/_ref). Test infrastructure, not product."""
@@ -68,5 +106,6 @@ def build_oracle() -> None:
 
 if __name__ == "__main__":
     build(verbose=True, force="--force" in sys.argv)
+    build_dropin(force="--force" in sys.argv)
     build_oracle()
     print(LIB)

@@ -103,6 +103,55 @@ void factor_tables(double* grow, double* shrink) {
     }
 }
 
+// Conservative sphere masks per orbital-plane angle bin (KParams::cull).
+// A plane through the camera-hole axis v with unit normal
+// n(theta) = cos(theta) a + sin(theta) b cuts sphere (c, r) iff
+// |ca cos(theta) + cb sin(theta)| < r, i.e. theta within asin(r / rho) of
+// atan2(cb, ca) + pi/2 (mod pi), rho = |(ca, cb)|. Each interval is widened
+// by two bins before marking. Returns false when culling is not applicable.
+constexpr int kCullBins = 4096;
+
+bool build_cull_table(const bhrt_scene* s, KParams& k, std::vector<unsigned long long>& table) {
+    if (s->integrator != BHRT_INTEGRATOR_RK4 && s->integrator != BHRT_INTEGRATOR_RKF45) return false;
+    const HV3 v = hsub(hv(s->cam_pos), hv(s->center));
+    if (hnorm(v) == 0.0) return false;
+    const HV3 vh = hnormalized(v);
+    // a: unit vector perpendicular to v, from the coordinate axis least aligned with it
+    HV3 axis = {1.0, 0.0, 0.0};
+    if (std::fabs(vh.y) < std::fabs(vh.x) && std::fabs(vh.y) <= std::fabs(vh.z)) axis = {0.0, 1.0, 0.0};
+    else if (std::fabs(vh.z) < std::fabs(vh.x)) axis = {0.0, 0.0, 1.0};
+    const HV3 a = hnormalized(hcross(vh, axis));
+    const HV3 b = hcross(vh, a);
+    const int words = (s->n_spheres + 63) / 64;
+    table.assign(static_cast<size_t>(kCullBins) * words, 0ull);
+    const double bw = kPi / kCullBins;
+    for (int i = 0; i < s->n_spheres; ++i) {
+        const HV3 c = hsub(hv(s->spheres[i].center), hv(s->center));
+        const double ca = hdot(c, a), cb = hdot(c, b);
+        const double rho = std::hypot(ca, cb);
+        const double r = s->spheres[i].radius;
+        const unsigned long long bit = 1ull << (i % 64);
+        const int w = i / 64;
+        if (rho <= r * (1.0 + 1e-9) + 1e-12) {
+            for (int j = 0; j < kCullBins; ++j) table[static_cast<size_t>(j) * words + w] |= bit;
+            continue;
+        }
+        const double half = std::asin(r / rho);
+        const double mid = std::atan2(cb, ca) + 0.5 * kPi;
+        const long lo = static_cast<long>(std::floor((mid - half) / bw)) - 2;
+        const long hi = static_cast<long>(std::floor((mid + half) / bw)) + 2;
+        for (long j = lo; j <= hi; ++j) {
+            const long jj = ((j % kCullBins) + kCullBins) % kCullBins;
+            table[static_cast<size_t>(jj) * words + w] |= bit;
+        }
+    }
+    hput(k.cull_a, a);
+    hput(k.cull_b, b);
+    k.cull_bins = kCullBins;
+    k.cull_words = words;
+    return true;
+}
+
 template <class T>
 struct DevBuf {
     T* p = nullptr;
@@ -141,6 +190,7 @@ struct bhrt_ctx {
     DevBuf<uint8_t> out;
     DevBuf<unsigned long long> stats;
     DevBuf<unsigned int> queue;
+    DevBuf<unsigned long long> cull;
     cudaStream_t last_stream = nullptr;
     int launches = 0;
     int pending = 0;
@@ -332,6 +382,7 @@ void bhrt_ctx_destroy(bhrt_ctx* c) {
     c->out.release();
     c->stats.release();
     c->queue.release();
+    c->cull.release();
     delete c;
 }
 
@@ -399,7 +450,15 @@ int bhrt_ctx_set_scene(bhrt_ctx* c, const bhrt_scene* s, bhrt_status_info* info)
         if (c->spheres.ensure(s->n_spheres)) return set_info(info, BHRT_DEVICE, -1, -1, "sphere alloc failed");
         CK(cudaMemcpy(c->spheres.p, s->spheres, sizeof(bhrt_sphere) * s->n_spheres, cudaMemcpyHostToDevice));
         k.spheres = c->spheres.p;
+        std::vector<unsigned long long> table;
+        if (build_cull_table(s, k, table)) {
+            if (c->cull.ensure(table.size())) return set_info(info, BHRT_DEVICE, -1, -1, "cull alloc failed");
+            CK(cudaMemcpy(c->cull.p, table.data(), sizeof(unsigned long long) * table.size(),
+                          cudaMemcpyHostToDevice));
+            k.cull = c->cull.p;
+        }
     }
+    k.fused_shade = (32 % s->spp) == 0 ? 1 : 0;
     k.grow = c->tables.p;
     k.shrink = c->tables.p + kQN;
     c->scene = *s;
@@ -426,7 +485,7 @@ int bhrt_ctx_render_async(bhrt_ctx* c, int32_t row_start, int32_t row_end, int32
     k.tile_offset = tile_offset;
     k.n_rows = rows;
     const size_t nrec = static_cast<size_t>(rows) * k.width * k.spp;
-    if (!d_records) {
+    if (!d_records && !k.fused_shade) {  // unfused shading reads the records
         if (c->records.ensure(nrec)) return set_info(info, BHRT_DEVICE, -1, -1, "records alloc failed");
         d_records = c->records.p;
     }
@@ -538,8 +597,14 @@ extern "C" int bhrt_cuda_render_rows(const bhrt_scene* s, int32_t row_start, int
         nrows[g] = bhrt_tile_row_count(row_start, row_end, tile_rows, G, g);
         if (ctxs[g]->out.ensure(3ull * nrows[g] * s->width + 1))
             return set_info(info, BHRT_DEVICE, -1, -1, "output alloc failed");
+        bhrt_ray_record* d_rec = nullptr;
+        if (records) {
+            if (ctxs[g]->records.ensure(static_cast<size_t>(nrows[g]) * s->width * s->spp))
+                return set_info(info, BHRT_DEVICE, -1, -1, "records alloc failed");
+            d_rec = ctxs[g]->records.p;
+        }
         rc = bhrt_ctx_render_async(ctxs[g], row_start, row_end, tile_rows, G, g, ctxs[g]->out.p,
-                                   nullptr, nullptr, info);
+                                   d_rec, nullptr, info);
         if (rc) return rc;
     }
     int first_fail = 0;

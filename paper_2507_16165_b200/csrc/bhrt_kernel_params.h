@@ -50,6 +50,18 @@ struct KParams {
     // RKF45 factor tables (device)
     const double* grow;
     const double* shrink;
+    // Sphere culling by orbital-plane angle. Every orbital plane contains the
+    // camera-hole axis v, so planes form a pencil n(theta) = cos(theta) a +
+    // sin(theta) b (a, b unit, perpendicular to v). cull[bin * cull_words + w]
+    // is a CONSERVATIVE mask of the spheres a plane with theta in the bin can
+    // cut; the exact fp64 test |c.n| < r still decides.
+    const unsigned long long* cull;
+    int32_t cull_bins, cull_words;
+    double cull_a[3], cull_b[3];
+    // 1: shade inside the trace kernel (spp divides 32; the spp samples of a
+    // pixel are adjacent lanes, summed in sample order by warp shuffles)
+    int32_t fused_shade;
+    int32_t pad2;
     // b-table (approximate mode)
     const double* table;
     int32_t table_entries, table_stride;

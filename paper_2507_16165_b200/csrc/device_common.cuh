@@ -154,16 +154,153 @@ struct SampleId {
     long long rec;  // record index
 };
 
+// Thread i -> (pixel, sample). Fused shading: the spp samples of a pixel are
+// adjacent lanes (i = pix*spp + s). Otherwise sample-major (i = s*plane + pix)
+// and a separate shade kernel reads the records.
 __device__ __forceinline__ SampleId sample_of(const KParams& p, long long i) {
     const long long plane = (long long)p.n_rows * p.width;
     SampleId id;
-    id.s = (int)(i / plane);
-    const long long pix = i - (long long)id.s * plane;
+    long long pix;
+    if (p.fused_shade) {
+        pix = i / p.spp;
+        id.s = (int)(i - pix * p.spp);
+    } else {
+        id.s = (int)(i / plane);
+        pix = i - (long long)id.s * plane;
+    }
     const int j = (int)(pix / p.width);
     id.x = (int)(pix - (long long)j * p.width);
     id.y = packed_row_to_y(p, j);
     id.rec = pix * p.spp + id.s;
     return id;
+}
+
+// ----------------------------------------------------------------- shading
+// image.cpp:131-169
+__device__ static __noinline__ void sample_direction(const KParams& p, V3 d, double out[3]) {
+    const double u_tex = (atan2(d.z, d.x) + PI_D) / (2.0 * PI_D);
+    const double v_tex = (PI_D / 2.0 - asin(clampd(d.y, -1.0, 1.0))) / PI_D;
+    const int w = p.sky_w, h = p.sky_h;
+    const double x = u_tex * w - 0.5;
+    const double y = v_tex * h - 0.5;
+    const double fx = x - floor(x);
+    const double fy = y - floor(y);
+    int i0 = (int)floor(x) % w;
+    if (i0 < 0) i0 += w;
+    int i1 = ((int)floor(x) + 1) % w;
+    if (i1 < 0) i1 += w;
+    int j0 = (int)floor(y);
+    j0 = j0 < 0 ? 0 : (j0 > h - 1 ? h - 1 : j0);
+    int j1 = (int)floor(y) + 1;
+    j1 = j1 < 0 ? 0 : (j1 > h - 1 ? h - 1 : j1);
+    const uint8_t* p00 = p.sky + 3 * ((size_t)j0 * w + i0);
+    const uint8_t* p10 = p.sky + 3 * ((size_t)j0 * w + i1);
+    const uint8_t* p01 = p.sky + 3 * ((size_t)j1 * w + i0);
+    const uint8_t* p11 = p.sky + 3 * ((size_t)j1 * w + i1);
+    const double w00 = (1.0 - fx) * (1.0 - fy);
+    const double w10 = fx * (1.0 - fy);
+    const double w01 = (1.0 - fx) * fy;
+    const double w11 = fx * fy;
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+        out[c] = (__ldg(p00 + c) * w00 + __ldg(p10 + c) * w10 + __ldg(p01 + c) * w01 +
+                  __ldg(p11 + c) * w11) / 255.0;
+}
+
+// Colour of one sample (oracle shade_object / sky): black for horizon and
+// stalled rays (render.cpp:30-34), sky, disk ramp, Lambertian sphere.
+__device__ static __noinline__ void shade_sample(const KParams& p, int obj, int sphere, V3 pt, double rgb[3]) {
+    rgb[0] = rgb[1] = rgb[2] = 0.0;
+    if (obj == BHRT_OBJ_SKY) {
+        if (p.sky_kind == BHRT_SKY_CHECKER) {
+            const double u_tex = (atan2(pt.z, pt.x) + PI_D) / (2.0 * PI_D);
+            const double v_tex = (PI_D / 2.0 - asin(clampd(pt.y, -1.0, 1.0))) / PI_D;
+            int cu = (int)floor(u_tex * p.checker_nu);
+            int cv = (int)floor(v_tex * p.checker_nv);
+            cu = cu < 0 ? 0 : (cu > p.checker_nu - 1 ? p.checker_nu - 1 : cu);
+            cv = cv < 0 ? 0 : (cv > p.checker_nv - 1 ? p.checker_nv - 1 : cv);
+            const double* c = ((cu + cv) & 1) ? p.checker_b : p.checker_a;
+            rgb[0] = c[0];
+            rgb[1] = c[1];
+            rgb[2] = c[2];
+        } else {
+            sample_direction(p, pt, rgb);
+        }
+    } else if (obj == BHRT_OBJ_DISK) {
+        const V3 q = sub(pt, vld(p.center));
+        const double rr = sqrt(q.x * q.x + q.z * q.z);
+        const double t = (rr - p.disk_r_in) / (p.disk_r_out - p.disk_r_in);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) rgb[c] = p.disk_c_in[c] + t * (p.disk_c_out[c] - p.disk_c_in[c]);
+    } else if (obj == BHRT_OBJ_SPHERE) {
+        const bhrt_sphere& sp = p.spheres[sphere];
+        const V3 nrm = dvd(sub(pt, vld(sp.center)), sp.radius);
+        const double lam = dmax(0.0, dot(nrm, vld(p.light)));
+        const double k = p.ambient + (1.0 - p.ambient) * lam;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) rgb[c] = sp.albedo[c] * k;
+    }
+}
+
+// render.cpp:42-48: inv = 1/spp, round-half-away-from-zero, clamp to [0,255].
+__device__ __forceinline__ void store_pixel(uint8_t* o, const double acc[3], int spp) {
+    const double inv = 1.0 / spp;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const double scaled = round(acc[c] * inv * 255.0);
+        o[c] = (uint8_t)clampd(scaled, 0.0, 255.0);
+    }
+}
+
+// Per-sample epilogue, called by EVERY lane of the warp (valid or not): the
+// optional record, and in fused mode the sample colour, the pixel sum in
+// sample order over the spp adjacent lanes (render.cpp:25-32) and the 8-bit
+// store. A failed sample fails its pixel (lowest failing pixel -> stats[3]).
+__device__ __forceinline__ void finish_sample(const KParams& p, bool valid, const SampleId& id, int obj,
+                                              int sphere, V3 point, double phi, unsigned steps,
+                                              unsigned rej) {
+    const bool has_point = obj == BHRT_OBJ_SKY || obj == BHRT_OBJ_DISK || obj == BHRT_OBJ_SPHERE;
+    if (valid && p.records) {
+        bhrt_ray_record rec;
+        rec.object = obj;
+        rec.sphere = sphere;
+        rec.steps = (int)steps;
+        rec.rejected = (int)rej;
+        rec.point[0] = has_point ? point.x : 0.0;
+        rec.point[1] = has_point ? point.y : 0.0;
+        rec.point[2] = has_point ? point.z : 0.0;
+        rec.phi = phi;
+        p.records[id.rec] = rec;
+    }
+    if (!p.fused_shade) return;
+    double rgb[3] = {0.0, 0.0, 0.0};
+    int bad = 0;
+    if (valid) {
+        if (obj < 0)
+            bad = 1;
+        else
+            shade_sample(p, obj, sphere, point, rgb);
+    }
+    const int lane = threadIdx.x & 31;
+    const int base = lane & ~(p.spp - 1);
+    double acc[3] = {0.0, 0.0, 0.0};
+    int anybad = 0;
+    for (int q = 0; q < p.spp; ++q) {
+        acc[0] += __shfl_sync(0xffffffffu, rgb[0], base + q);
+        acc[1] += __shfl_sync(0xffffffffu, rgb[1], base + q);
+        acc[2] += __shfl_sync(0xffffffffu, rgb[2], base + q);
+        anybad |= __shfl_sync(0xffffffffu, bad, base + q);
+    }
+    if (valid && id.s == 0) {
+        const long long pix = id.rec / p.spp;
+        uint8_t* o = p.out + 3 * pix;
+        if (anybad) {
+            atomicMin(&p.stats[3], (unsigned long long)pix);
+            o[0] = o[1] = o[2] = 0;
+        } else {
+            store_pixel(o, acc, p.spp);
+        }
+    }
 }
 
 // ================================================================= RK4 / RKF45 scene modes

@@ -118,19 +118,18 @@ __global__ void __launch_bounds__(128) trace_reference_kernel(const __grid_const
     const long long n = (long long)p.n_rows * p.width * p.spp;
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     unsigned nsteps = 0, nrej = 0;
-    if (i < n) {
-        const SampleId id = sample_of(p, i);
-        bhrt_ray_record rec;
-        rec.sphere = -1;
-        rec.point[0] = rec.point[1] = rec.point[2] = 0.0;
-        rec.phi = 0.0;
+    const bool valid = i < n;
+    const SampleId id = sample_of(p, valid ? i : 0);
+    int obj = BHRT_OBJ_NONE;
+    V3 edir = mk(0.0, 0.0, 0.0);
+    double phi_end = 0.0;
+    if (valid) {
         const V3 origin = vld(p.cam_pos), center = vld(p.center);
         const V3 dir = camera_ray(p, id.x, id.y, id.s);
         const V3 v = sub(origin, center);
         const double r0 = norm(v);
         const Basis B = plane_basis(origin, dir, center);
-        int obj;
-        V3 edir = dir;
+        edir = dir;
         if (!B.ok) {  // radial: geodesic.cpp:175-187
             obj = dot(dir, sub(center, origin)) > 0.0 ? BHRT_OBJ_HORIZON : BHRT_OBJ_SKY;
             (void)r0;
@@ -168,19 +167,11 @@ __global__ void __launch_bounds__(128) trace_reference_kernel(const __grid_const
                 last_u = u;
                 ++npts;
             }
-            rec.phi = phi;
+            phi_end = phi;
         }
-        rec.object = obj;
-        if (obj == BHRT_OBJ_SKY) {
-            rec.point[0] = edir.x;
-            rec.point[1] = edir.y;
-            rec.point[2] = edir.z;
-        }
-        rec.steps = (int)nsteps;
-        rec.rejected = (int)nrej;
-        p.records[id.rec] = rec;
     }
-    warp_add_stats(p.stats, nsteps, nrej, i < n ? 1ull : 0ull);
+    finish_sample(p, valid, id, obj, -1, edir, phi_end, nsteps, nrej);
+    warp_add_stats(p.stats, nsteps, nrej, valid ? 1ull : 0ull);
 }
 
 void launch_reference(const KParams& p, cudaStream_t st) {

@@ -16,7 +16,7 @@ constexpr int kSlots = 8;
 constexpr int kSphSm = 128;          // spheres staged in shared memory
 constexpr float kWinMargin = 5e-4f;  // fp32 window slack (rad); windows only cull
 #ifndef BHRT_SCENE_MINB
-#define BHRT_SCENE_MINB 5  // min resident blocks per SM (register cap), tuned on B200
+#define BHRT_SCENE_MINB 4  // min resident blocks per SM (register cap), tuned on B200
 #endif
 
 struct SceneSm {
@@ -85,23 +85,15 @@ __device__ double events_setup(const KParams& p, SceneSm& sm, int t, V3 e1, V3 e
     sm.next_disk[t] = next_disk;
     int nc = 0;
     float next_sph = CUDART_INF_F;
-    const float nxf = (float)n.x, nyf = (float)n.y, nzf = (float)n.z;
-    const int ns = p.n_spheres;
-    for (int k = 0; k < ns; ++k) {
-        bool maybe = true;
-        if (k < kSphSm) {  // conservative fp32 prefilter; the fp64 test below decides
-            const float4 f = sm.sph[k];
-            const float dnf = f.x * nxf + f.y * nyf + f.z * nzf;
-            maybe = fabsf(dnf) < f.w;
-        }
-        if (!maybe) continue;
+    // exact fp64 candidate test (oracle: |c.n| < r), in increasing sphere order
+    auto consider = [&](int k) -> bool {
         const V3 c = sphere_c(p, k);
         const double r = __ldg(&p.spheres[k].radius);
         const double dn = dot(c, n);
-        if (!(fabs(dn) < r)) continue;
+        if (!(fabs(dn) < r)) return true;
         if (nc == kSlots) {
             nc = -1;
-            break;
+            return false;
         }
         const double cx = dot(c, e1), cy = dot(c, e2);
         const double rho2 = r * r - dn * dn;
@@ -112,6 +104,37 @@ __device__ double events_setup(const KParams& p, SceneSm& sm, int t, V3 e1, V3 e
         sm.k[nc][t] = (unsigned char)k;
         next_sph = fminf(next_sph, lo);
         ++nc;
+        return true;
+    };
+    const int ns = p.n_spheres;
+    if (p.cull && ns > 0) {
+        // plane-angle bin -> conservative sphere mask (host table, KParams::cull)
+        const float na = (float)(n.x * p.cull_a[0] + n.y * p.cull_a[1] + n.z * p.cull_a[2]);
+        const float nb = (float)(n.x * p.cull_b[0] + n.y * p.cull_b[1] + n.z * p.cull_b[2]);
+        float th = atan2f(nb, na);
+        if (th < 0.0f) th += (float)PI_D;
+        int bin = (int)(th * (float)(p.cull_bins / PI_D));
+        bin = bin < 0 ? 0 : (bin >= p.cull_bins ? p.cull_bins - 1 : bin);
+        const unsigned long long* row = p.cull + (size_t)bin * p.cull_words;
+        bool go = true;
+        for (int w = 0; w < p.cull_words && go; ++w) {
+            unsigned long long m = __ldg(row + w);
+            while (m && go) {
+                const int k = w * 64 + __ffsll((long long)m) - 1;
+                m &= m - 1;
+                go = consider(k);
+            }
+        }
+    } else {
+        const float nxf = (float)n.x, nyf = (float)n.y, nzf = (float)n.z;
+        for (int k = 0; k < ns; ++k) {
+            if (k < kSphSm) {  // conservative fp32 prefilter; the fp64 test decides
+                const float4 f = sm.sph[k];
+                const float dnf = f.x * nxf + f.y * nyf + f.z * nzf;
+                if (!(fabsf(dnf) < f.w)) continue;
+            }
+            if (!consider(k)) break;
+        }
     }
     if (nc < 0) next_sph = -CUDART_INF_F;
     sm.nc[t] = nc;
@@ -376,16 +399,17 @@ __global__ void __launch_bounds__(kBlock, BHRT_SCENE_MINB) trace_scene_kernel(co
     const long long n = (long long)p.n_rows * p.width * p.spp;
     const long long i = (long long)blockIdx.x * blockDim.x + t;
     unsigned nsteps = 0, nrej = 0;
-    if (i < n) {
-        const SampleId id = sample_of(p, i);
+    const bool valid = i < n;
+    const SampleId id = sample_of(p, valid ? i : 0);
+    Hit H;
+    H.obj = BHRT_OBJ_NONE;
+    H.sphere = -1;
+    H.point = mk(0.0, 0.0, 0.0);
+    double phi = 0.0;
+    if (valid) {
         const V3 origin = vld(p.cam_pos), O = vld(p.center);
         const V3 dir = camera_ray(p, id.x, id.y, id.s);
         const Basis B = plane_basis(origin, dir, O);
-        Hit H;
-        H.obj = BHRT_OBJ_NONE;
-        H.sphere = -1;
-        H.point = mk(0.0, 0.0, 0.0);
-        double phi = 0.0;
         if (!B.ok) {
             const double r0 = norm(sub(origin, O));
             const bool cap = dot(dir, sub(O, origin)) > 0.0;
@@ -459,19 +483,9 @@ __global__ void __launch_bounds__(kBlock, BHRT_SCENE_MINB) trace_scene_kernel(co
             }
             if (H.obj == BHRT_OBJ_SKY) H.point = escape_dir(p, sm, t, has_step, pp, up, wp, phi, u, w);
         }
-        bhrt_ray_record rec;
-        rec.object = H.obj;
-        rec.sphere = H.sphere;
-        const bool has_point = H.obj == BHRT_OBJ_SKY || H.obj == BHRT_OBJ_DISK || H.obj == BHRT_OBJ_SPHERE;
-        rec.point[0] = has_point ? H.point.x : 0.0;
-        rec.point[1] = has_point ? H.point.y : 0.0;
-        rec.point[2] = has_point ? H.point.z : 0.0;
-        rec.phi = phi;
-        rec.steps = (int)nsteps;
-        rec.rejected = (int)nrej;
-        p.records[id.rec] = rec;
     }
-    warp_add_stats(p.stats, nsteps, nrej, i < n ? 1ull : 0ull);
+    finish_sample(p, valid, id, H.obj, H.sphere, H.point, phi, nsteps, nrej);
+    warp_add_stats(p.stats, nsteps, nrej, valid ? 1ull : 0ull);
 }
 
 void launch_scene(const KParams& p, cudaStream_t st) {
