@@ -634,6 +634,8 @@ typedef struct {
     cam_t cam;
     double u_cap, u_esc, phi_max, M3;
     v3 light;
+    orc_table* table;  /* approximate mode: the b-table ... */
+    double* psi0;      /* ... and each entry's inbound psi of the camera's u0 */
 } prep_t;
 
 static int prep_scene(const bhrt_scene* s, prep_t* p) {
@@ -645,6 +647,8 @@ static int prep_scene(const bhrt_scene* s, prep_t* p) {
     p->phi_max = 2.0 * PI * s->max_windings;
     p->M3 = 3.0 * s->mass;
     p->light = normalized(vld(s->light_dir));
+    p->table = NULL;
+    p->psi0 = NULL;
     return 0;
 }
 
@@ -1002,6 +1006,293 @@ static int trace_scene(const bhrt_scene* s, const prep_t* P, v3 origin, v3 dir, 
     return 0;
 }
 
+/* ------------------------------------------------------------------ */
+/* Approximate mode: b-table of inbound orbits      */
+/* ------------------------------------------------------------------ */
+struct orc_table {
+    int entries, ns;
+    double b_max, dpsi, u_cap, u_esc;
+    int* kind;
+    int* n;
+    double* ends; /* psi_end, u_end, w_end, psi_esc */
+    double* smp;  /* entries * ns * 2 */
+};
+
+static inline double hermite_ddeval(const double a[4], double t) { return fma(6.0 * a[3], t, 2.0 * a[2]); }
+
+/* Newton on H(t) = target (or H'(t) = 0 when deriv) from t0, 3 iterations, clamped. */
+static double cubic_solve(const double a[4], double t, double target, int deriv) {
+    for (int it = 0; it < 3; ++it) {
+        const double f = deriv ? hermite_deval(a, t) : hermite_eval(a, t) - target;
+        const double df = deriv ? hermite_ddeval(a, t) : hermite_deval(a, t);
+        if (df != 0.0) t = t - f / df;
+        t = clampd(t, 0.0, 1.0);
+    }
+    return t;
+}
+
+static void table_entry_build(const bhrt_scene* s, orc_table* T, int e) {
+    const double b = T->b_max * e / (T->entries - 1);
+    double* S = T->smp + (size_t)e * T->ns * 2;
+    double* E = T->ends + 4 * (size_t)e;
+    if (!(b > 0.0)) {
+        T->kind[e] = 3;
+        T->n[e] = 0;
+        E[0] = E[1] = E[2] = 0.0;
+        E[3] = -1.0;
+        return;
+    }
+    const double M3 = 3.0 * s->mass;
+    double u = 0.0, w = 1.0 / b, psi = 0.0, h = s->step;
+    S[0] = u;
+    S[1] = w;
+    int cnt = 1, kind = 2;
+    for (;;) {
+        if (cnt >= T->ns) { E[0] = psi; E[1] = u; E[2] = w; break; }
+        const double target = (double)cnt * T->dpsi;
+        int done = 0;
+        while (psi < target) {
+            const double rem = target - psi;
+            const int last = !(h < rem);
+            const double ht = last ? rem : h;
+            double un, wn, hn;
+            const int acc = rkf45_step(u, w, ht, M3, s->rel_tol, s->abs_tol, s->max_step, &un, &wn, &hn);
+            if (acc) {
+                if (un >= T->u_cap || wn <= 0.0) {
+                    double a[4];
+                    hermite_coef(ht, u, w, un, wn, a);
+                    if (un >= T->u_cap) { /* capture inside this step */
+                        const double t = cubic_solve(a, (T->u_cap - u) / (un - u), T->u_cap, 0);
+                        E[0] = psi + ht * t; E[1] = T->u_cap; E[2] = hermite_deval(a, t) / ht;
+                        kind = 0;
+                    } else { /* periapsis u' = 0 inside this step */
+                        const double t = cubic_solve(a, w / (w - wn), 0.0, 1);
+                        E[0] = psi + ht * t; E[1] = hermite_eval(a, t); E[2] = 0.0;
+                        kind = 1;
+                    }
+                    done = 1;
+                    break;
+                }
+                psi = last ? target : psi + ht;
+                u = un;
+                w = wn;
+            }
+            h = hn;
+            if (h < 1e-14) { E[0] = psi; E[1] = u; E[2] = w; done = 1; break; }
+        }
+        if (done) break;
+        S[2 * cnt] = u;
+        S[2 * cnt + 1] = w;
+        ++cnt;
+    }
+    T->kind[e] = kind;
+    T->n[e] = cnt;
+    E[3] = -1.0;
+    E[3] = orc_table_inbound_psi(T, e, T->u_esc);
+}
+
+double orc_table_inbound_psi(const orc_table* T, int e, double target) {
+    const int kind = T->kind[e], n = T->n[e];
+    if (kind == 3 || n < 1) return -1.0;
+    const double* S = T->smp + (size_t)e * T->ns * 2;
+    const double* E = T->ends + 4 * (size_t)e;
+    if (!(target > S[0])) return 0.0;
+    int j;
+    double h, ua, wa, ub, wb;
+    if (!(S[2 * (n - 1)] > target)) { /* at or beyond the last sample: end segment */
+        if (kind == 2 || E[1] < target) return -1.0;
+        j = n - 1;
+        h = E[0] - (double)j * T->dpsi;
+        ua = S[2 * j]; wa = S[2 * j + 1]; ub = E[1]; wb = E[2];
+        if (!(h > 0.0)) return E[0];
+    } else {
+        int lo = 0, hi = n - 1; /* u(lo) <= target < u(hi) */
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) / 2;
+            if (S[2 * mid] <= target) lo = mid; else hi = mid;
+        }
+        j = lo;
+        h = T->dpsi;
+        ua = S[2 * j]; wa = S[2 * j + 1]; ub = S[2 * j + 2]; wb = S[2 * j + 3];
+    }
+    double a[4];
+    hermite_coef(h, ua, wa, ub, wb, a);
+    const double t0 = ub > ua ? (target - ua) / (ub - ua) : 0.0;
+    const double t = cubic_solve(a, t0, target, 0);
+    return (double)j * T->dpsi + h * t;
+}
+
+/* u on entry e at orbit angle psi (mirror beyond periapsis); -1 if undefined. */
+static double table_u(const orc_table* T, int e, double psi) {
+    const int kind = T->kind[e], n = T->n[e];
+    const double* S = T->smp + (size_t)e * T->ns * 2;
+    const double* E = T->ends + 4 * (size_t)e;
+    if (kind == 1 && psi > E[0]) psi = 2.0 * E[0] - psi;
+    if (psi < 0.0 || n < 1) return -1.0;
+    int j = (int)floor(psi / T->dpsi);
+    double h, ua, wa, ub, wb, pa;
+    if (j >= n - 1) {
+        if (kind == 2 || psi > E[0]) return -1.0;
+        j = n - 1;
+        pa = (double)j * T->dpsi;
+        h = E[0] - pa;
+        if (!(h > 0.0)) return E[1];
+        ua = S[2 * j]; wa = S[2 * j + 1]; ub = E[1]; wb = E[2];
+    } else {
+        pa = (double)j * T->dpsi;
+        h = T->dpsi;
+        ua = S[2 * j]; wa = S[2 * j + 1]; ub = S[2 * j + 2]; wb = S[2 * j + 3];
+    }
+    double a[4];
+    hermite_coef(h, ua, wa, ub, wb, a);
+    return hermite_eval(a, (psi - pa) / h);
+}
+
+orc_table* orc_table_build(const bhrt_scene* s) {
+    pthread_once(&g_tables_once, make_tables);
+    if (s->table_entries < 2 || s->table_samples < 2 || !(s->table_b_max > 0.0) || !(s->table_dpsi > 0.0))
+        return NULL;
+    orc_table* T = (orc_table*)calloc(1, sizeof *T);
+    T->entries = s->table_entries;
+    T->ns = s->table_samples;
+    T->b_max = s->table_b_max;
+    T->dpsi = s->table_dpsi;
+    T->u_cap = s->mass > 0.0 ? 1.0 / (2.0 * s->mass) : INFINITY;
+    T->u_esc = 1.0 / s->escape_radius;
+    T->kind = (int*)calloc((size_t)T->entries, sizeof(int));
+    T->n = (int*)calloc((size_t)T->entries, sizeof(int));
+    T->ends = (double*)calloc((size_t)T->entries * 4, sizeof(double));
+    T->smp = (double*)calloc((size_t)T->entries * T->ns * 2, sizeof(double));
+    for (int e = 0; e < T->entries; ++e) table_entry_build(s, T, e);
+    return T;
+}
+
+void orc_table_free(orc_table* T) {
+    if (!T) return;
+    free(T->kind); free(T->n); free(T->ends); free(T->smp); free(T);
+}
+
+int orc_table_entry(const orc_table* T, int e, int* kind, int* n, double ends[4], double* samples, int cap) {
+    if (!T || e < 0 || e >= T->entries) return BHRT_INVALID_ARGUMENT;
+    *kind = T->kind[e];
+    *n = T->n[e];
+    memcpy(ends, T->ends + 4 * (size_t)e, 4 * sizeof(double));
+    const int m = T->n[e] < cap ? T->n[e] : cap;
+    if (samples) memcpy(samples, T->smp + (size_t)e * T->ns * 2, 2 * sizeof(double) * (size_t)m);
+    return 0;
+}
+
+/* One entry's plan for a ray with camera-side inbound position psi0. */
+static int table_plan(const orc_table* T, int e, double psi0, double w0, int* outcome, double* phi_end) {
+    const int kind = T->kind[e];
+    const double* E = T->ends + 4 * (size_t)e;
+    if (kind == 3 || psi0 < 0.0) return 0;
+    if (w0 >= 0.0) { /* moving inward along the orbit */
+        if (kind == 0) { *outcome = BHRT_OBJ_HORIZON; *phi_end = E[0] - psi0; return 1; }
+        if (kind == 2) { *outcome = BHRT_OBJ_STALLED; *phi_end = INFINITY; return 1; }
+        if (E[3] < 0.0) return 0;
+        *outcome = BHRT_OBJ_SKY;
+        *phi_end = (2.0 * E[0] - E[3]) - psi0;
+        return 1;
+    }
+    if (E[3] < 0.0) return 0; /* moving outward: straight back out along the inbound branch */
+    *outcome = BHRT_OBJ_SKY;
+    *phi_end = psi0 - E[3];
+    return 1;
+}
+
+static int trace_table(const bhrt_scene* s, const prep_t* P, v3 origin, v3 dir, bhrt_ray_record* rec,
+                       scene_ray_t* R) {
+    const orc_table* T = P->table;
+    R->s = s;
+    R->O = vld(s->center);
+    R->obj = BHRT_OBJ_NONE;
+    R->sphere = -1;
+    rec->steps = 0;
+    rec->rejected = 0;
+    rec->phi = 0.0;
+    const double o[3] = {origin.x, origin.y, origin.z}, d[3] = {dir.x, dir.y, dir.z};
+    double e1a[3], e2a[3];
+    if (!orc_plane_basis(o, d, s->center, e1a, e2a)) {
+        const double r0 = norm(sub(origin, R->O));
+        const int cap = dot(dir, sub(R->O, origin)) > 0.0;
+        radial_scene(R, origin, dir, cap ? r0 - 2.0 * s->mass : s->escape_radius, cap);
+        return 0;
+    }
+    R->e1 = vld(e1a);
+    R->e2 = vld(e2a);
+    R->n = cross(R->e1, R->e2);
+    double st[3];
+    orc_initial_conditions(o, d, s->center, st);
+    const double u0 = st[1], w0 = st[2];
+    const double M2 = 2.0 * s->mass;
+    const double energy = w0 * w0 + u0 * u0 - M2 * u0 * u0 * u0;
+    /* The orbit's impact parameter is fixed by its first integral
+     * u'^2 + u^2 - 2Mu^3 = 1/b^2 (geodesic.cpp:272-275), not by |v x d|: the
+     * initial conditions (geodesic.cpp:57-65) are flat-space ones. */
+    if (!(energy > 0.0)) { R->obj = BHRT_OBJ_STALLED; return 0; } /* never reaches infinity */
+    const double b = 1.0 / sqrt(energy);
+    ray_events_setup(R);
+    const int N = T->entries;
+    const double x = (b * (double)(N - 1)) / T->b_max;
+    int i = (int)floor(x);
+    if (i > N - 2) i = N - 2;
+    double f = x - (double)i;
+    if (T->kind[i] == 3) f = 1.0;
+    int oi = 0, oj = 0;
+    double pi_ = 0.0, pj = 0.0;
+    const int vi = table_plan(T, i, P->psi0[i], w0, &oi, &pi_);
+    const int vj = table_plan(T, i + 1, P->psi0[i + 1], w0, &oj, &pj);
+    int outcome;
+    double phi_end, wi, wj;
+    if (vi && vj && oi == oj && f > 0.0 && f < 1.0) {
+        outcome = oi;
+        phi_end = outcome == BHRT_OBJ_STALLED ? INFINITY : (1.0 - f) * pi_ + f * pj;
+        wi = 1.0 - f;
+        wj = f;
+    } else {
+        int use_j = f >= 0.5;
+        if (use_j && !vj) use_j = 0;
+        if (!use_j && !vi) use_j = 1;
+        if (use_j ? !vj : !vi) { R->obj = BHRT_OBJ_STALLED; return 0; }
+        outcome = use_j ? oj : oi;
+        phi_end = use_j ? pj : pi_;
+        wi = use_j ? 0.0 : 1.0;
+        wj = use_j ? 1.0 : 0.0;
+    }
+    if (phi_end > P->phi_max) outcome = BHRT_OBJ_STALLED;
+    const double stop = outcome == BHRT_OBJ_STALLED ? P->phi_max : phi_end;
+    const double sgn = w0 >= 0.0 ? 1.0 : -1.0;
+    while (R->next_disk < stop) { /* disk events along the interpolated orbit */
+        const double ph = R->next_disk;
+        double ui = -1.0, uj = -1.0;
+        if (wi > 0.0) ui = table_u(T, i, P->psi0[i] + sgn * ph);
+        if (wj > 0.0) uj = table_u(T, i + 1, P->psi0[i + 1] + sgn * ph);
+        double u_ev;
+        if (wi > 0.0 && wj > 0.0 && ui >= 0.0 && uj >= 0.0) u_ev = wi * ui + wj * uj;
+        else u_ev = ui >= 0.0 ? ui : uj;
+        if (u_ev > 0.0) {
+            const double r_ev = 1.0 / u_ev;
+            if (r_ev >= s->disk_r_in && r_ev <= s->disk_r_out) {
+                R->obj = BHRT_OBJ_DISK;
+                R->point = add(R->O, scl(R->disk_L, R->disk_sigma * r_ev));
+                rec->phi = ph;
+                return 0;
+            }
+        }
+        R->next_disk += PI;
+        R->disk_sigma = -R->disk_sigma;
+    }
+    R->obj = outcome;
+    rec->phi = outcome == BHRT_OBJ_STALLED ? P->phi_max : phi_end;
+    if (outcome == BHRT_OBJ_SKY) {
+        const double ue = P->u_esc;
+        const double q = energy - ue * ue + M2 * ue * ue * ue;
+        R->point = tangent_dir(R, phi_end, ue, -sqrt(q > 0.0 ? q : 0.0));
+    }
+    return 0;
+}
+
 static void shade_object(const bhrt_scene* s, const prep_t* P, const scene_ray_t* R, double rgb[3]) {
     rgb[0] = rgb[1] = rgb[2] = 0.0;
     switch (R->obj) {
@@ -1052,7 +1343,8 @@ static int trace_sample_prepared(const bhrt_scene* s, const prep_t* P, int px, i
         return 0;
     }
     scene_ray_t R;
-    const int rc = trace_scene(s, P, origin, dir, rec, &R);
+    const int rc = s->integrator == BHRT_INTEGRATOR_TABLE ? trace_table(s, P, origin, dir, rec, &R)
+                                                          : trace_scene(s, P, origin, dir, rec, &R);
     if (rc) return rc;
     rec->object = R.obj;
     rec->sphere = R.sphere;
@@ -1062,12 +1354,47 @@ static int trace_sample_prepared(const bhrt_scene* s, const prep_t* P, int px, i
     return 0;
 }
 
+/* The b-table depends only on these scene fields; the last one built is cached. */
+static pthread_mutex_t g_table_mu = PTHREAD_MUTEX_INITIALIZER;
+static orc_table* g_table = NULL;
+static double g_table_key[10];
+
+static int prep_table(const bhrt_scene* s, prep_t* P) {
+    if (s->integrator != BHRT_INTEGRATOR_TABLE) return 0;
+    const double key[10] = {s->mass, s->rel_tol, s->abs_tol, s->step, s->max_step,
+                            (double)s->table_entries, (double)s->table_samples, s->table_b_max,
+                            s->table_dpsi, s->escape_radius};
+    pthread_mutex_lock(&g_table_mu);
+    if (!g_table || memcmp(key, g_table_key, sizeof key) != 0) {
+        orc_table_free(g_table);
+        g_table = orc_table_build(s);
+        memcpy(g_table_key, key, sizeof key);
+    }
+    P->table = g_table;
+    pthread_mutex_unlock(&g_table_mu);
+    if (!P->table) return BHRT_INVALID_ARGUMENT;
+    /* bind the camera radius: each entry's inbound psi of u0 = 1/|cam - O| */
+    const double u0 = 1.0 / norm(sub(vld(s->cam_pos), vld(s->center)));
+    P->psi0 = (double*)malloc(sizeof(double) * (size_t)P->table->entries);
+    for (int e = 0; e < P->table->entries; ++e) P->psi0[e] = orc_table_inbound_psi(P->table, e, u0);
+    return 0;
+}
+
+static void prep_release(prep_t* P) {
+    free(P->psi0);
+    P->psi0 = NULL;
+}
+
 int orc_trace_sample(const bhrt_scene* s, int px, int py, int sample, bhrt_ray_record* rec,
                      double rgb[3]) {
     prep_t P;
-    const int st = prep_scene(s, &P);
+    int st = prep_scene(s, &P);
     if (st) return st;
-    return trace_sample_prepared(s, &P, px, py, sample, rec, rgb);
+    st = prep_table(s, &P);
+    if (st) return st;
+    st = trace_sample_prepared(s, &P, px, py, sample, rec, rgb);
+    prep_release(&P);
+    return st;
 }
 
 static int shade_prepared(const bhrt_scene* s, const prep_t* P, int px, int py, uint8_t out[3],
@@ -1093,9 +1420,13 @@ static int shade_prepared(const bhrt_scene* s, const prep_t* P, int px, int py, 
 
 int orc_shade_pixel(const bhrt_scene* s, int px, int py, uint8_t out[3], bhrt_ray_record* recs) {
     prep_t P;
-    const int st = prep_scene(s, &P);
+    int st = prep_scene(s, &P);
     if (st) return st;
-    return shade_prepared(s, &P, px, py, out, recs);
+    st = prep_table(s, &P);
+    if (st) return st;
+    st = shade_prepared(s, &P, px, py, out, recs);
+    prep_release(&P);
+    return st;
 }
 
 void orc_scene_defaults(bhrt_scene* s) {
@@ -1171,6 +1502,9 @@ static int validate_trace(const bhrt_scene* s, bhrt_status_info* info) {
         (s->integrator != BHRT_INTEGRATOR_REFERENCE && !(s->step > 0.0)) ||
         (s->integrator == BHRT_INTEGRATOR_RKF45 && !(s->max_step > 0.0 && s->max_step < 1.0)) ||
         (s->integrator == BHRT_INTEGRATOR_REFERENCE && (s->disk_enabled || s->n_spheres > 0)) ||
+        (s->integrator == BHRT_INTEGRATOR_TABLE &&
+         (s->n_spheres > 0 || s->table_entries < 2 || s->table_samples < 2 || !(s->table_b_max > 0.0) ||
+          !(s->table_dpsi > 0.0) || !(s->max_step > 0.0 && s->max_step < 1.0))) ||
         !(s->chord_dphi > 0.0) || (s->n_spheres > 0 && s->spheres == NULL) ||
         (s->sky_kind == BHRT_SKY_CHECKER && (s->checker_nu < 1 || s->checker_nv < 1))) {
         set_info(info, BHRT_INVALID_ARGUMENT, -1, -1, "scene extension: invalid parameter");
@@ -1251,6 +1585,11 @@ int orc_render_rows(const bhrt_scene* s, int row_start, int row_end, int threads
     if (rc) return rc;
     prep_t P;
     prep_scene(s, &P);
+    rc = prep_table(s, &P);
+    if (rc) {
+        set_info(info, rc, -1, -1, "table: invalid parameters");
+        return rc;
+    }
     job_t J = {s, &P, row_start, row_end, out, records, row_start, PTHREAD_MUTEX_INITIALIZER, 0, 0, 0};
     const int rows = row_end - row_start;
     const int pool = threads < rows ? threads : rows;
@@ -1262,6 +1601,7 @@ int orc_render_rows(const bhrt_scene* s, int row_start, int row_end, int threads
         for (int i = 0; i < pool; ++i) pthread_join(ts[i], NULL);
         free(ts);
     }
+    prep_release(&P);
     if (J.fail_code) {
         char msg[128];
         snprintf(msg, sizeof msg, "pixel (%d, %d): numerical failure", J.fail_px, J.fail_py);

@@ -98,12 +98,19 @@ int orc_make_spheres(uint64_t seed, int n, const double center[3], double shell_
                      double shell_max, double radius_min, double radius_max, bhrt_sphere* out);
 void orc_scene_defaults(bhrt_scene* s);
 
-/* Approximate mode (config 3): b-table build + lookup. Layout documented in
- * DESIGN.md §Table. */
-int orc_table_build(const bhrt_scene* s, double* table, int64_t table_len);
-int64_t orc_table_len(const bhrt_scene* s);
-/* Uses the table previously built (set with orc_table_use). */
-void orc_table_use(const double* table);
+/* Approximate mode (config 3): a table of INBOUND null
+ * orbits u(psi) for b_e = table_b_max * e / (table_entries - 1), sampled at
+ * psi_j = j * table_dpsi by RKF45 (scene tolerances), ending at capture
+ * (u = 1/2M) or periapsis (u' = 0). Per entry: kind (0 captured, 1 escaping,
+ * 2 undecided/truncated, 3 radial b = 0), n samples, ends = {psi_end, u_end,
+ * w_end, psi_esc}, samples = (u, u') pairs. */
+typedef struct orc_table orc_table;
+orc_table* orc_table_build(const bhrt_scene* s);
+void orc_table_free(orc_table* t);
+int orc_table_entry(const orc_table* t, int e, int* kind, int* n, double ends[4], double* samples,
+                    int cap);
+/* Inbound psi where u = target on entry e (Hermite + Newton), -1 if unreachable. */
+double orc_table_inbound_psi(const orc_table* t, int e, double target);
 
 #ifdef __cplusplus
 }

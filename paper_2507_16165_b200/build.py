@@ -24,7 +24,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # (DESIGN.md §Parity).
 NVFLAGS = ["-O3", "-std=c++17", "-lineinfo", "--fmad=false", "-Xptxas", "-v",
            "-Xcompiler", "-fPIC,-ffp-contract=off,-O2", "-I" + os.path.join(ROOT, "include")]
-SOURCES = ["trace_reference.cu", "trace_scene.cu", "shade.cu", "bhrt_cuda.cu", "fp64_peak.cu"]
+SOURCES = ["trace_reference.cu", "trace_scene.cu", "table.cu", "shade.cu", "bhrt_cuda.cu",
+           "fp64_peak.cu"]
 
 
 def _stale(target: str, deps: list[str]) -> bool:

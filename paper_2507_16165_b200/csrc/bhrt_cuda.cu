@@ -21,6 +21,8 @@
 namespace bhrt_b200 {
 
 int launch_trace(const KParams& p, cudaStream_t st, int* launches, cudaEvent_t* ev);
+void launch_table_build(const KParams& p, double* smp, double* ends, int32_t* kind, int32_t* n, cudaStream_t st);
+void launch_table_bind(const KParams& p, double* ends, double* psi0, double u0, cudaStream_t st);
 
 namespace {
 
@@ -83,6 +85,9 @@ int validate_trace(const bhrt_scene* s, bhrt_status_info* info) {
         (s->integrator != BHRT_INTEGRATOR_REFERENCE && !(s->step > 0.0)) ||
         (s->integrator == BHRT_INTEGRATOR_RKF45 && !(s->max_step > 0.0 && s->max_step < 1.0)) ||
         (s->integrator == BHRT_INTEGRATOR_REFERENCE && (s->disk_enabled || s->n_spheres > 0)) ||
+        (s->integrator == BHRT_INTEGRATOR_TABLE &&
+         (s->n_spheres > 0 || s->table_entries < 2 || s->table_samples < 2 || !(s->table_b_max > 0.0) ||
+          !(s->table_dpsi > 0.0) || !(s->max_step > 0.0 && s->max_step < 1.0))) ||
         !(s->chord_dphi > 0.0) || (s->n_spheres > 0 && s->spheres == nullptr) ||
         s->n_spheres < 0 || s->n_spheres > kMaxSpheres ||
         (s->sky_kind == BHRT_SKY_CHECKER && (s->checker_nu < 1 || s->checker_nv < 1)))
@@ -191,6 +196,10 @@ struct bhrt_ctx {
     DevBuf<unsigned long long> stats;
     DevBuf<unsigned int> queue;
     DevBuf<unsigned long long> cull;
+    DevBuf<double> tab_smp, tab_ends, tab_psi0;
+    DevBuf<int32_t> tab_kind, tab_n;
+    bool has_table = false;
+    double table_key[10] = {0};
     cudaStream_t last_stream = nullptr;
     int launches = 0;
     int pending = 0;
@@ -383,6 +392,11 @@ void bhrt_ctx_destroy(bhrt_ctx* c) {
     c->stats.release();
     c->queue.release();
     c->cull.release();
+    c->tab_smp.release();
+    c->tab_ends.release();
+    c->tab_psi0.release();
+    c->tab_kind.release();
+    c->tab_n.release();
     delete c;
 }
 
@@ -391,8 +405,6 @@ int bhrt_ctx_set_scene(bhrt_ctx* c, const bhrt_scene* s, bhrt_status_info* info)
     if (rc) return rc;
     rc = validate_trace(s, info);
     if (rc) return rc;
-    if (s->integrator == BHRT_INTEGRATOR_TABLE)
-        return set_info(info, BHRT_INVALID_ARGUMENT, -1, -1, "table integrator not built in this version");
     CK(cudaSetDevice(c->device));
     CK(cudaDeviceSynchronize());
     KParams& k = c->kp;
@@ -459,6 +471,37 @@ int bhrt_ctx_set_scene(bhrt_ctx* c, const bhrt_scene* s, bhrt_status_info* info)
         }
     }
     k.fused_shade = (32 % s->spp) == 0 ? 1 : 0;
+    if (s->integrator == BHRT_INTEGRATOR_TABLE) {
+        // The b-table depends only on these fields; rebuild only when they change.
+        const double key[10] = {s->mass, s->rel_tol, s->abs_tol, s->step, s->max_step,
+                                (double)s->table_entries, (double)s->table_samples, s->table_b_max,
+                                s->table_dpsi, s->escape_radius};
+        k.table_entries = s->table_entries;
+        k.table_ns = s->table_samples;
+        k.table_b_max = s->table_b_max;
+        k.table_dpsi = s->table_dpsi;
+        const size_t E = static_cast<size_t>(s->table_entries);
+        if (!c->has_table || std::memcmp(key, c->table_key, sizeof key) != 0) {
+            if (c->tab_smp.ensure(E * s->table_samples * 2) || c->tab_ends.ensure(E * 4) ||
+                c->tab_kind.ensure(E) || c->tab_n.ensure(E) || c->tab_psi0.ensure(E))
+                return set_info(info, BHRT_DEVICE, -1, -1, "table alloc failed");
+            launch_table_build(k, c->tab_smp.p, c->tab_ends.p, c->tab_kind.p, c->tab_n.p, nullptr);
+            CK(cudaGetLastError());
+            CK(cudaDeviceSynchronize());
+            std::memcpy(c->table_key, key, sizeof key);
+            c->has_table = true;
+        }
+        k.tab_smp = c->tab_smp.p;
+        k.tab_ends = c->tab_ends.p;
+        k.tab_kind = c->tab_kind.p;
+        k.tab_n = c->tab_n.p;
+        k.tab_psi0 = c->tab_psi0.p;
+        // bind the frame: each entry's inbound psi of the camera's u0 (oracle prep_table)
+        const double u0 = 1.0 / hnorm(hsub(hv(s->cam_pos), hv(s->center)));
+        launch_table_bind(k, c->tab_ends.p, c->tab_psi0.p, u0, nullptr);
+        CK(cudaGetLastError());
+        CK(cudaDeviceSynchronize());
+    }
     k.grow = c->tables.p;
     k.shrink = c->tables.p + kQN;
     c->scene = *s;

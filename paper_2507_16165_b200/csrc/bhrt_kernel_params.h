@@ -62,10 +62,16 @@ struct KParams {
     // pixel are adjacent lanes, summed in sample order by warp shuffles)
     int32_t fused_shade;
     int32_t pad2;
-    // b-table (approximate mode)
-    const double* table;
-    int32_t table_entries, table_stride;
-    double table_b_max, table_db, table_dpsi;
+    // b-table (approximate mode): per entry kind/n, ends
+    // {psi_end, u_end, w_end, psi_esc}, (u, u') samples at psi_j = j*dpsi with
+    // a fixed stride of table_ns samples, and the frame's inbound psi of u0.
+    const double* tab_smp;
+    const double* tab_ends;
+    const int32_t* tab_kind;
+    const int32_t* tab_n;
+    const double* tab_psi0;
+    int32_t table_entries, table_ns;
+    double table_b_max, table_dpsi;
     // outputs
     bhrt_ray_record* records;   // n_rows * width * spp
     uint8_t* out;               // n_rows * width * 3

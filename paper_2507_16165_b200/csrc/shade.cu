@@ -37,17 +37,18 @@ __global__ void __launch_bounds__(256) shade_kernel(const __grid_constant__ KPar
 
 void launch_reference(const KParams& p, cudaStream_t st);
 void launch_scene(const KParams& p, cudaStream_t st);
+void launch_table_trace(const KParams& p, cudaStream_t st);
 
 int launch_trace(const KParams& p, cudaStream_t st, int* launches, cudaEvent_t* ev) {
     const long long n = (long long)p.n_rows * p.width * p.spp;
     if (n <= 0) return 0;
-    if (p.integrator != BHRT_INTEGRATOR_REFERENCE && p.integrator != BHRT_INTEGRATOR_RK4 &&
-        p.integrator != BHRT_INTEGRATOR_RKF45)
-        return -1;
+    if (p.integrator < BHRT_INTEGRATOR_REFERENCE || p.integrator > BHRT_INTEGRATOR_TABLE) return -1;
     if (!p.fused_shade && !p.records) return -1;
     if (ev) cudaEventRecord(ev[0], st);
     if (p.integrator == BHRT_INTEGRATOR_REFERENCE)
         launch_reference(p, st);
+    else if (p.integrator == BHRT_INTEGRATOR_TABLE)
+        launch_table_trace(p, st);
     else
         launch_scene(p, st);
     ++*launches;

@@ -149,3 +149,13 @@ def ref_render(scene, rows=None, threads=8):
     info = StatusInfo()
     rc = L.ref_render_rows(C.byref(scene), r0, r1, threads, u8p(out), C.byref(info))
     return rc, out, info
+
+
+def table_entry(t, e, cap=4096):
+    L = oracle()
+    kind, n = C.c_int(), C.c_int()
+    ends = dbuf(4)
+    smp = dbuf(2 * cap)
+    rc = L.orc_table_entry(t, e, C.byref(kind), C.byref(n), ends, smp, cap)
+    assert rc == 0
+    return kind.value, n.value, list(ends), np.array(list(smp)[:2 * n.value]).reshape(-1, 2)

@@ -68,6 +68,29 @@ def test_scene_modes_match_oracle(idx, w, h):
     assert res["steps_equal"]
 
 
+def test_table_mode_matches_oracle():
+    """Approximate mode (config 3 scene, smaller frame and table): GPU b-table
+    build + lookup vs the oracle's."""
+    sb = scenes.config(3, 96, 54)
+    sb.s.table_entries = 20000
+    compare(sb)
+
+
+def test_table_mode_close_to_direct_integration():
+    """config 3's own check: table lookup vs direct RKF45 on the same pixels."""
+    tab = scenes.config(3, 160, 90)
+    direct = scenes.config(1, 160, 90)
+    a, ra = render.render_rows(tab, 0, 90, 1, records=True)
+    b, rb = render.render_rows(direct, 0, 90, 1, records=True)
+    same = ra["object"] == rb["object"]
+    assert same.mean() >= 0.995
+    hit = same & np.isin(ra["object"], [OBJ_SKY, OBJ_DISK])
+    err = np.abs(ra["point"][hit] - rb["point"][hit]).max(axis=1)
+    assert np.median(err) < 1e-5
+    diff = np.abs(a.astype(int) - b.astype(int)).reshape(-1, 3).max(axis=1)
+    assert (diff > 0).mean() < 0.01
+
+
 def test_row_tiles_assemble_to_full_frame():
     sb = scenes.config(2, 64, 40)
     full = render.render_image(sb).reshape(40, -1)

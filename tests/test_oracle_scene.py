@@ -177,3 +177,22 @@ def test_rk4_image_close_to_reference_sky_only_image():
     assert rc == 0
     diff = np.abs(img.astype(int) - ref_img.astype(int)).reshape(-1, 3).max(1)
     assert (diff > 8).mean() < 0.03  # bilinear blur at cell edges only
+
+
+def test_table_mode_flat_space_exact_and_close_to_direct():
+    """Approximate mode (config 3): flat space reproduces straight lines; with
+    M = 1 the table agrees with direct RKF45 integration except near the
+    critical impact parameter / disk edges (table resolution)."""
+    for mass in (0.0, 1.0):
+        tab = scenes.config(3, 64, 36)
+        tab.set(mass=mass, table_entries=20000)
+        direct = scenes.config(1, 64, 36)
+        direct.set(mass=mass)
+        ia, oa, pa, _, _ = recs(tab)
+        ib, ob, pb, _, _ = recs(direct)
+        assert (oa != ob).mean() <= 0.005
+        both = (oa == ob) & np.isin(oa, [OBJ_SKY, OBJ_DISK])
+        err = np.abs(pa[both] - pb[both]).max(axis=1)
+        assert np.median(err) < 1e-5
+        if mass == 0.0:
+            assert err.max() < 1e-5

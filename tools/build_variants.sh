@@ -9,7 +9,7 @@ FL="-O3 -std=c++17 -lineinfo --fmad=false -Xcompiler -fPIC,-ffp-contract=off -Ii
 for spec in "$@"; do   # spec: name:-DFOO=1,-DBAR=2
   name=${spec%%:*}; defs=${spec#*:}; defs=${defs//,/ }
   objs=""
-  for f in trace_reference trace_scene shade bhrt_cuda fp64_peak; do
+  for f in trace_reference trace_scene table shade bhrt_cuda fp64_peak; do
     nvcc $ARCH $FL $defs -c paper_2507_16165_b200/csrc/$f.cu -o build/variants/${name}_$f.o
     objs="$objs build/variants/${name}_$f.o"
   done
