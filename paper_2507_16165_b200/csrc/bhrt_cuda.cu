@@ -471,6 +471,8 @@ int bhrt_ctx_set_scene(bhrt_ctx* c, const bhrt_scene* s, bhrt_status_info* info)
         }
     }
     k.fused_shade = (32 % s->spp) == 0 ? 1 : 0;
+    k.grow = c->tables.p;
+    k.shrink = c->tables.p + kQN;
     if (s->integrator == BHRT_INTEGRATOR_TABLE) {
         // The b-table depends only on these fields; rebuild only when they change.
         const double key[10] = {s->mass, s->rel_tol, s->abs_tol, s->step, s->max_step,

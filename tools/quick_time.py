@@ -12,10 +12,10 @@ def main():
     idx = int(sys.argv[1]) if len(sys.argv) > 1 else 2
     reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
     sb = scenes.config(idx)
-    if idx == 3:
-        sb = scenes.config(1, 7680, 4320)
     ctx = render.Context(0)
+    t0 = time.time()
     ctx.set_scene(sb)
+    print(f"set_scene (incl. table build for config 3): {time.time() - t0:.3f} s", flush=True)
     out = torch.empty(sb.s.height * sb.s.width * 3, dtype=torch.uint8, device="cuda")
     st = torch.cuda.current_stream()
     for r in range(reps + 1):
