@@ -419,6 +419,13 @@ int bhrt_ctx_set_scene(bhrt_ctx* c, const bhrt_scene* s, bhrt_status_info* info)
     k.max_windings = s->max_windings;
     k.integrator = s->integrator;
     std::memcpy(k.cam_pos, s->cam_pos, sizeof k.cam_pos);
+    {  // per-frame constants of plane_basis / initial_conditions (geodesic.cpp:49-65)
+        const HV3 v = hsub(hv(s->cam_pos), hv(s->center));
+        hput(k.cam_v, v);
+        hput(k.cam_e1, hnormalized(v));
+        k.cam_r0 = hnorm(v);
+        k.cam_u0 = 1.0 / k.cam_r0;
+    }
     HV3 f, r, u;
     camera_basis(s, f, r, u);
     hput(k.forward, f);

@@ -22,7 +22,8 @@ struct KParams {
     double u_cap, u_esc, phi_max, escape_radius;
     int32_t max_windings;
     int32_t integrator;
-    // camera (hoisted)
+    // camera (hoisted): v = cam_pos - center, e1 = v/|v|, r0 = |v|, u0 = 1/r0
+    double cam_v[3], cam_e1[3], cam_r0, cam_u0;
     double cam_pos[3];
     double forward[3], right[3], up[3];
     double tan_half_x, tan_half_y;

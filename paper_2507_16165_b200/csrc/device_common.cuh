@@ -115,23 +115,26 @@ struct Basis {
     bool ok;
 };
 
-// geodesic.cpp:49-55
-__device__ __forceinline__ Basis plane_basis(V3 origin, V3 dir, V3 center) {
+// geodesic.cpp:49-55. Every camera ray starts at the camera, so
+// e1 = normalized(origin - center) is a per-frame constant (KParams::cam_e1,
+// computed on the host with the same operations).
+__device__ __forceinline__ Basis plane_basis(const KParams& p, V3 dir) {
     Basis b;
-    b.e1 = normalized(sub(origin, center));
+    b.e1 = vld(p.cam_e1);
     const V3 tangential = sub(dir, scl(b.e1, dot(dir, b.e1)));
-    b.ok = !(norm(tangential) < 1e-12);
-    b.e2 = b.ok ? normalized(tangential) : mk(0, 0, 0);
+    const double tn = norm(tangential);
+    b.ok = !(tn < 1e-12);
+    b.e2 = b.ok ? dvd(tangential, tn) : mk(0, 0, 0);
     return b;
 }
 
-// geodesic.cpp:57-65 (called only with a non-radial ray)
-__device__ __forceinline__ void initial_conditions(V3 origin, V3 dir, V3 center, double& u, double& w) {
-    const V3 v = sub(origin, center);
-    const double r0 = norm(v);
+// geodesic.cpp:57-65 (called only with a non-radial ray); v = origin - center,
+// r0 = |v| and u0 = 1/r0 are per-frame constants (KParams::cam_v/cam_r0/cam_u0).
+__device__ __forceinline__ void initial_conditions(const KParams& p, V3 dir, double& u, double& w) {
+    const V3 v = vld(p.cam_v);
     const double b = norm(cross(v, dir));
-    u = 1.0 / r0;
-    w = -dot(v, dir) / (r0 * b);
+    u = p.cam_u0;
+    w = -dot(v, dir) / (p.cam_r0 * b);
 }
 
 // ----------------------------------------------------------------- record / stats helpers

@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(128) trace_table_kernel(const __grid_constant_
         const TabView T{p.tab_smp, p.tab_ends, p.tab_kind, p.tab_n, p.table_ns, p.table_dpsi};
         const V3 origin = vld(p.cam_pos), O = vld(p.center);
         const V3 dir = camera_ray(p, id.x, id.y, id.s);
-        const Basis B = plane_basis(origin, dir, O);
+        const Basis B = plane_basis(p, dir);
         if (!B.ok) {  // radial: straight segment (geodesic.cpp:175-187); table mode has no spheres
             const double r0 = norm(sub(origin, O));
             const bool cap = dot(dir, sub(O, origin)) > 0.0;
@@ -271,7 +271,7 @@ __global__ void __launch_bounds__(128) trace_table_kernel(const __grid_constant_
         } else {
             const V3 e1 = B.e1, e2 = B.e2, nrm = cross(e1, e2);
             double u0, w0;
-            initial_conditions(origin, dir, O, u0, w0);
+            initial_conditions(p, dir, u0, w0);
             const double M2 = 2.0 * p.mass;
             const double energy = w0 * w0 + u0 * u0 - M2 * u0 * u0 * u0;
             if (!(energy > 0.0)) {

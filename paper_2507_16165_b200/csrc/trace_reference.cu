@@ -128,14 +128,14 @@ __global__ void __launch_bounds__(128) trace_reference_kernel(const __grid_const
         const V3 dir = camera_ray(p, id.x, id.y, id.s);
         const V3 v = sub(origin, center);
         const double r0 = norm(v);
-        const Basis B = plane_basis(origin, dir, center);
+        const Basis B = plane_basis(p, dir);
         edir = dir;
         if (!B.ok) {  // radial: geodesic.cpp:175-187
             obj = dot(dir, sub(center, origin)) > 0.0 ? BHRT_OBJ_HORIZON : BHRT_OBJ_SKY;
             (void)r0;
         } else {
             double u, w, phi = 0.0, hint = 0.0;
-            initial_conditions(origin, dir, center, u, w);
+            initial_conditions(p, dir, u, w);
             double prev_phi = 0.0, prev_u = 0.0, last_phi = 0.0, last_u = 0.0;
             int npts = 1;
             obj = BHRT_OBJ_NONE;

@@ -194,8 +194,9 @@ __device__ __noinline__ bool step_events(const KParams& p, SceneSm& sm, int t, d
         int S = 1;
         if (h > p.chord_dphi) S = (int)ceil(h / p.chord_dphi);
         const double dl = h / S;
-        const double cd_ = cos(dl), sd_ = sin(dl);
-        const double c0 = cos(pa), s0 = sin(pa);
+        double cd_, sd_, c0, s0;
+        sincos(dl, &sd_, &cd_);
+        sincos(pa, &s0, &c0);
         const float fpa = (float)pa, fdl = (float)dl;
         int best_j = S;
         double best_t = CUDART_INF;
@@ -315,7 +316,8 @@ __device__ __noinline__ bool step_events(const KParams& p, SceneSm& sm, int t, d
 }
 
 __device__ __forceinline__ V3 tangent_dir(V3 e1, V3 e2, double phi, double u, double w) {
-    const double c = cos(phi), sn = sin(phi);
+    double c, sn;
+    sincos(phi, &sn, &c);
     const double tx = -u * sn - w * c, ty = u * c - w * sn;
     return normalized(add(scl(e1, tx), scl(e2, ty)));
 }
@@ -409,7 +411,7 @@ __global__ void __launch_bounds__(kBlock, BHRT_SCENE_MINB) trace_scene_kernel(co
     if (valid) {
         const V3 origin = vld(p.cam_pos), O = vld(p.center);
         const V3 dir = camera_ray(p, id.x, id.y, id.s);
-        const Basis B = plane_basis(origin, dir, O);
+        const Basis B = plane_basis(p, dir);
         if (!B.ok) {
             const double r0 = norm(sub(origin, O));
             const bool cap = dot(dir, sub(O, origin)) > 0.0;
@@ -420,7 +422,7 @@ __global__ void __launch_bounds__(kBlock, BHRT_SCENE_MINB) trace_scene_kernel(co
             st3(sm.e2, t, B.e2);
             st3(sm.n, t, nrm);
             double u, w;
-            initial_conditions(origin, dir, O, u, w);
+            initial_conditions(p, dir, u, w);
             sm.energy[t] = w * w + u * u - (2.0 * p.mass) * u * u * u;
             double next_ev = events_setup(p, sm, t, B.e1, B.e2, nrm);
             double pp = 0.0, up = 0.0, wp = 0.0;  // state before the last accepted step
