@@ -164,14 +164,20 @@ __device__ __forceinline__ SampleId sample_of(const KParams& p, long long i) {
     const long long plane = (long long)p.n_rows * p.width;
     SampleId id;
     long long pix;
-    if (p.fused_shade) {
-        pix = i / p.spp;
-        id.s = (int)(i - pix * p.spp);
+    if (p.fused_shade) {  // spp divides 32: a power of two, so a shift
+        const int sh = __ffs(p.spp) - 1;
+        pix = i >> sh;
+        id.s = (int)(i & (p.spp - 1));
     } else {
         id.s = (int)(i / plane);
         pix = i - (long long)id.s * plane;
     }
-    const int j = (int)(pix / p.width);
+    int j;
+    if (pix < 0x7fffffffLL) {  // 32-bit division when it fits (it does for 8K frames)
+        j = (int)((unsigned)pix / (unsigned)p.width);
+    } else {
+        j = (int)(pix / p.width);
+    }
     id.x = (int)(pix - (long long)j * p.width);
     id.y = packed_row_to_y(p, j);
     id.rec = pix * p.spp + id.s;

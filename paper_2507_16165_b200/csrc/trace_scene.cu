@@ -53,7 +53,7 @@ __device__ __forceinline__ void sphere_window_f(double cx, double cy, double rho
         hi = CUDART_INF_F;
         return;
     }
-    const float a = atan2f((float)sqrt(rho2), (float)sqrt(q));  // asin(rho / rc)
+    const float a = atan2f(sqrtf((float)rho2), sqrtf((float)q));  // asin(rho / rc)
     const float pc = atan2f((float)cy, (float)cx);
     lo = pc - a - kWinMargin;
     hi = pc + a + kWinMargin;
@@ -197,7 +197,7 @@ __device__ __noinline__ bool step_events(const KParams& p, SceneSm& sm, int t, d
         double cd_, sd_, c0, s0;
         sincos(dl, &sd_, &cd_);
         sincos(pa, &s0, &c0);
-        const float fpa = (float)pa, fdl = (float)dl;
+        const float fpa = (float)pa, rdl = 1.0f / (float)dl;  // conservative range only
         int best_j = S;
         double best_t = CUDART_INF;
         const int ncand = test_all ? p.n_spheres : nc;
@@ -210,8 +210,8 @@ __device__ __noinline__ bool step_events(const KParams& p, SceneSm& sm, int t, d
                 k = sm.k[a][t];
                 // clamp in float first: windows may be infinite
                 const float fS = (float)S;
-                j0 = (int)fminf(fmaxf(floorf((sm.lo[a][t] - fpa) / fdl) - 1.0f, 0.0f), fS);
-                j1 = (int)fminf(fmaxf(floorf((sm.hi[a][t] - fpa) / fdl) + 1.0f, 0.0f), fS - 1.0f);
+                j0 = (int)fminf(fmaxf(floorf((sm.lo[a][t] - fpa) * rdl) - 1.0f, 0.0f), fS);
+                j1 = (int)fminf(fmaxf(floorf((sm.hi[a][t] - fpa) * rdl) + 1.0f, 0.0f), fS - 1.0f);
             }
             j1 = min(j1, best_j);
             if (j0 > j1) continue;
