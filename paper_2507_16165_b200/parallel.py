@@ -85,6 +85,17 @@ class FrameRenderer:
                               stream=st.cuda_stream)
         if self.world == 1:
             return self.out.view(h, w, 3)
+        if dist.get_backend(self.group) != "nccl":
+            # host-staged gather (gloo: CPU tests / ranks sharing one GPU)
+            self.ctx.finish()
+            mine = self.out.cpu()
+            if self.rank == 0:
+                gl = [torch.empty_like(mine) for _ in range(self.world)]
+                dist.gather(mine, gl, dst=0, group=self.group)
+                return assemble(torch.stack(gl).to(self.out.device), h, w, self.world,
+                                self.tile_rows)
+            dist.gather(mine, None, dst=0, group=self.group)
+            return None
         with torch.cuda.stream(st):
             if self.rank == 0:
                 dist.gather(self.out, list(self.gathered.unbind(0)), dst=0, group=self.group)
