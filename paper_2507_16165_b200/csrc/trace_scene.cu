@@ -26,7 +26,8 @@ struct SceneSm {
     double dl[2][kBlock];  // unit disk line, orbital-plane coordinates
     double dL[2][kBlock];  // unit disk line, world x and z (y = 0)
     double sigma[kBlock], energy[kBlock], next_disk[kBlock];
-    float lo[kSlots][kBlock], hi[kSlots][kBlock];
+    float lo[kSlots][kBlock], hi[kSlots][kBlock];   // angular window (unwrapped phi)
+    float rlo[kSlots][kBlock], rhi[kSlots][kBlock]; // radial extent of the circle
     unsigned char k[kSlots][kBlock];
     int nc[kBlock];
     float next_sph[kBlock];
@@ -101,6 +102,9 @@ __device__ double events_setup(const KParams& p, SceneSm& sm, int t, V3 e1, V3 e
         sphere_window_f(cx, cy, rho2, lo, hi);
         sm.lo[nc][t] = lo;
         sm.hi[nc][t] = hi;
+        const float rc = sqrtf((float)(cx * cx + cy * cy)), rho = sqrtf((float)rho2);
+        sm.rlo[nc][t] = (rc - rho) * 0.999f - 1e-3f;
+        sm.rhi[nc][t] = (rc + rho) * 1.001f + 1e-3f;
         sm.k[nc][t] = (unsigned char)k;
         next_sph = fminf(next_sph, lo);
         ++nc;
@@ -178,8 +182,18 @@ __device__ __noinline__ bool step_events(const KParams& p, SceneSm& sm, int t, d
     unsigned act = 0;
     if (!test_all) {
         const float fa = (float)pa, fb = (float)pb;
+        // conservative radial extent of the step's polyline: monotone u (same
+        // sign of u' at both ends) keeps it within the end radii, widened 2%
+        // for chord sagitta (h <= 0.1 rad) and interpolant overshoot
+        const float ra = 1.0f / (float)ua, rb = 1.0f / (float)ub;
+        float slo = 0.0f, shi = CUDART_INF_F;
+        if ((wa > 0.0) == (wb > 0.0) && h <= 0.1) {
+            slo = fminf(ra, rb) * 0.98f;
+            shi = fmaxf(ra, rb) * 1.02f;
+        }
         for (int i = 0; i < nc; ++i)
-            if (sm.lo[i][t] <= fb && sm.hi[i][t] >= fa) act |= 1u << i;
+            if (sm.lo[i][t] <= fb && sm.hi[i][t] >= fa && sm.rlo[i][t] <= shi && sm.rhi[i][t] >= slo)
+                act |= 1u << i;
     }
     bool sph_hit = false;
     int bsph = -1;
