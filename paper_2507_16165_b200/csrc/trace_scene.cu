@@ -23,8 +23,6 @@ struct SceneSm {
     float4 sph[kSphSm];  // (cx, cy, cz, r + fp32 slack) relative to the hole: cull prefilter
     double grow[kQN], shrink[kQN];
     double e1[3][kBlock], e2[3][kBlock], n[3][kBlock];
-    double dl[2][kBlock];  // unit disk line, orbital-plane coordinates
-    double dL[2][kBlock];  // unit disk line, world x and z (y = 0)
     double sigma[kBlock], energy[kBlock], next_disk[kBlock];
     float lo[kSlots][kBlock], hi[kSlots][kBlock];   // angular window (unwrapped phi)
     float rlo[kSlots][kBlock], rhi[kSlots][kBlock]; // radial extent of the circle
@@ -54,7 +52,13 @@ __device__ __forceinline__ void sphere_window_f(double cx, double cy, double rho
         hi = CUDART_INF_F;
         return;
     }
-    const float a = atan2f(sqrtf((float)rho2), sqrtf((float)q));  // asin(rho / rc)
+    // half-width asin(x), x = rho/rc, bounded from above without a second
+    // atan2: asin(x) <= x (1 + x^2/5) on [0, 1/2] (series 1/6 + 3x^2/40 + ...),
+    // and <= pi/2 beyond.
+    const float rcf = sqrtf((float)(cx * cx + cy * cy));
+    const float x = sqrtf((float)rho2) / rcf;
+    const float a = x <= 0.5f ? x * (1.0f + 0.2f * x * x) * 1.0001f : 1.5708f;
+    (void)q;
     const float pc = atan2f((float)cy, (float)cx);
     lo = pc - a - kWinMargin;
     hi = pc + a + kWinMargin;
@@ -77,10 +81,7 @@ __device__ double events_setup(const KParams& p, SceneSm& sm, int t, V3 e1, V3 e
             const double pl = atan2(ly, lx);
             next_disk = pl > 0.0 ? pl : pl + PI_D;
             sm.sigma[t] = pl > 0.0 ? 1.0 : -1.0;
-            sm.dl[0][t] = lx / nl;
-            sm.dl[1][t] = ly / nl;
-            sm.dL[0][t] = L.x / nl;
-            sm.dL[1][t] = L.z / nl;
+            // the unit line (lx/nl, ly/nl) and L/nl are formed at hit time (disk_line)
         }
     }
     sm.next_disk[t] = next_disk;
@@ -151,6 +152,17 @@ struct Hit {
     V3 point;
 };
 
+// Unit disk line in plane coordinates and world space (oracle ray_events_setup
+// values, same operations), formed only when a disk crossing lands in the annulus.
+__device__ __forceinline__ void disk_line(const SceneSm& sm, int t, double& dlx, double& dly, V3& Lw) {
+    const V3 n = ld3(sm.n, t), e1 = ld3(sm.e1, t), e2 = ld3(sm.e2, t);
+    const V3 L = mk(-n.z, 0.0, n.x);
+    const double nl = norm(L);
+    dlx = dot(L, e1) / nl;
+    dly = dot(L, e2) / nl;
+    Lw = dvd(L, nl);
+}
+
 // Oracle step_events(): disk = exact phi-event on the step's Hermite
 // interpolant; spheres = first entering hit on S equal-angle sub-chords.
 // Returns true on hit; always advances the event state and next_ev.
@@ -163,6 +175,7 @@ __device__ __noinline__ bool step_events(const KParams& p, SceneSm& sm, int t, d
     // ---- disk
     bool disk_hit = false;
     double r_ev = 0.0, dlx = 0.0, dly = 0.0;
+    V3 Lw = mk(0.0, 0.0, 0.0);
     const double sigma = sm.sigma[t];
     if (next_disk > pa && next_disk <= pb) {
         const double tt = (next_disk - pa) / h;
@@ -171,8 +184,10 @@ __device__ __noinline__ bool step_events(const KParams& p, SceneSm& sm, int t, d
             r_ev = 1.0 / u_ev;
             if (r_ev >= p.disk_r_in && r_ev <= p.disk_r_out) {
                 disk_hit = true;
-                dlx = sigma * sm.dl[0][t];
-                dly = sigma * sm.dl[1][t];
+                double ux, uy;
+                disk_line(sm, t, ux, uy, Lw);
+                dlx = sigma * ux;
+                dly = sigma * uy;
             }
         }
     }
@@ -291,7 +306,6 @@ __device__ __noinline__ bool step_events(const KParams& p, SceneSm& sm, int t, d
     if (disk_hit) {
         hit.obj = BHRT_OBJ_DISK;
         hit.sphere = -1;
-        const V3 Lw = mk(sm.dL[0][t], 0.0, sm.dL[1][t]);
         hit.point = add(vld(p.center), scl(Lw, sigma * r_ev));
     } else if (sph_hit) {
         hit.obj = BHRT_OBJ_SPHERE;
