@@ -204,7 +204,7 @@ struct bhrt_ctx {
     int launches = 0;
     int pending = 0;
     int32_t last_rows = 0;
-    unsigned long long host_stats[4] = {0, 0, 0, 0};
+    unsigned long long host_stats[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     bool timing = false;
     bool timed = false;
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
@@ -347,7 +347,7 @@ int bhrt_ctx_create(int32_t device, bhrt_ctx** out, bhrt_status_info* info) {
     CK(cudaSetDevice(device));
     std::unique_ptr<bhrt_ctx> c(new bhrt_ctx());
     c->device = device;
-    if (c->stats.ensure(4) || c->queue.ensure(1) || c->tables.ensure(2 * kQN))
+    if (c->stats.ensure(8) || c->queue.ensure(1) || c->tables.ensure(2 * kQN))
         return set_info(info, BHRT_DEVICE, -1, -1, "bhrt_ctx_create: cudaMalloc failed");
     double tb[2 * kQN];
     factor_tables(tb, tb + kQN);
@@ -545,7 +545,7 @@ int bhrt_ctx_render_async(bhrt_ctx* c, int32_t row_start, int32_t row_end, int32
     k.out = d_out;
     k.stats = c->stats.p;
     k.queue = c->queue.p;
-    const unsigned long long init[4] = {0ull, 0ull, 0ull, ULLONG_MAX};
+    const unsigned long long init[8] = {0ull, 0ull, 0ull, ULLONG_MAX, 0ull, 0ull, 0ull, 0ull};
     CK(cudaMemcpyAsync(c->stats.p, init, sizeof init, cudaMemcpyHostToDevice, st));
     CK(cudaMemsetAsync(c->queue.p, 0, sizeof(unsigned int), st));
     c->launches = 0;
@@ -582,6 +582,12 @@ int bhrt_ctx_finish(bhrt_ctx* c, bhrt_status_info* info) {
         std::snprintf(msg, sizeof msg, "pixel (%d, %d): numerical failure", px, py);
         return set_info(info, BHRT_NUMERICAL, px, py, msg);
     }
+    return 0;
+}
+
+int bhrt_ctx_counters(bhrt_ctx* c, uint64_t out[8]) {
+    if (!c) return BHRT_INVALID_ARGUMENT;
+    for (int i = 0; i < 8; ++i) out[i] = c->host_stats[i];
     return 0;
 }
 

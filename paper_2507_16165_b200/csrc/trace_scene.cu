@@ -142,6 +142,9 @@ __device__ double events_setup(const KParams& p, SceneSm& sm, int t, V3 e1, V3 e
         }
     }
     if (nc < 0) next_sph = -CUDART_INF_F;
+#ifdef BHRT_COUNTERS
+    atomicAdd(&p.stats[6], (unsigned long long)(nc < 0 ? 100 : nc));
+#endif
     sm.nc[t] = nc;
     sm.next_sph[t] = next_sph;
     return dmin(next_disk, (double)next_sph);
@@ -172,6 +175,9 @@ __device__ __noinline__ bool step_events(const KParams& p, SceneSm& sm, int t, d
     const double h = pb - pa;
     const Cubic cu = hermite_coef(h, ua, wa, ub, wb);
     double next_disk = sm.next_disk[t];
+#ifdef BHRT_COUNTERS
+    atomicAdd(&p.stats[7], 1ull);
+#endif
     // ---- disk
     bool disk_hit = false;
     double r_ev = 0.0, dlx = 0.0, dly = 0.0;
@@ -219,12 +225,21 @@ __device__ __noinline__ bool step_events(const KParams& p, SceneSm& sm, int t, d
         // overlaps and stops at its first hit; the winner is the
         // lexicographic minimum of (sub-chord, chord parameter), ties to the
         // lower slot — the same hit the oracle finds.
-        const V3 e1 = ld3(sm.e1, t), e2 = ld3(sm.e2, t), n = ld3(sm.n, t);
         int S = 1;
         if (h > p.chord_dphi) S = (int)ceil(h / p.chord_dphi);
         const double dl = h / S;
         double cd_, sd_, c0, s0;
-        sincos(dl, &sd_, &cd_);
+        if (dl <= 0.02) {
+            // sub-chord rotation: Taylor series, truncation < 1e-20 for dl <= 0.02
+            // (the oracle calls cos/sin; both are correctly rounded to ~1 ulp)
+            const double d2 = dl * dl;
+            cd_ = fma(fma(fma(fma(d2, -1.0 / 3628800.0, 1.0 / 40320.0), d2, -1.0 / 720.0), d2, 1.0 / 24.0),
+                      d2 * d2, fma(d2, -0.5, 1.0));
+            sd_ = fma(fma(fma(fma(d2, 1.0 / 362880.0, -1.0 / 5040.0), d2, 1.0 / 120.0), d2, -1.0 / 6.0),
+                      d2 * dl, dl);
+        } else {
+            sincos(dl, &sd_, &cd_);
+        }
         sincos(pa, &s0, &c0);
         const float fpa = (float)pa, rdl = 1.0f / (float)dl;  // conservative range only
         int best_j = S;
@@ -244,11 +259,12 @@ __device__ __noinline__ bool step_events(const KParams& p, SceneSm& sm, int t, d
             }
             j1 = min(j1, best_j);
             if (j0 > j1) continue;
+            const V3 e1 = ld3(sm.e1, t), e2 = ld3(sm.e2, t), n = ld3(sm.n, t);
             const V3 c = sphere_c(p, k);
             const double r = __ldg(&p.spheres[k].radius);
             const double dn = dot(c, n);
             if (!(fabs(dn) < r)) continue;
-            const double ccx = dot(c, e1), ccy = dot(c, e2);
+            const double ccx = dot(c, e1), ccy = dot(c, e2);  // = the oracle's cand_t values
             const double rho2 = r * r - dn * dn;
             double cj = c0, sj = s0;
             for (int j = 0; j < j0; ++j) {  // same recurrence values as the sequential walk
@@ -294,8 +310,13 @@ __device__ __noinline__ bool step_events(const KParams& p, SceneSm& sm, int t, d
         }
         sph_hit = best_j < S;
         if (sph_hit) {
+            const V3 e1 = ld3(sm.e1, t), e2 = ld3(sm.e2, t);
             hit.point = add(vld(p.center), add(scl(e1, bqx), scl(e2, bqy)));
         }
+#ifdef BHRT_COUNTERS
+        atomicAdd(&p.stats[4], 1ull);
+        atomicAdd(&p.stats[5], (unsigned long long)__popc(act));
+#endif
     }
     if (sph_hit && disk_hit) {
         if (bqx * dly - bqy * dlx > 0.0)

@@ -174,6 +174,11 @@ class Context:
             raise native.BhrtError(rc, -1, -1, "kernel timing unavailable")
         return a.value, b.value
 
+    def counters(self) -> list[int]:
+        out = (C.c_uint64 * 8)()
+        native.lib().bhrt_ctx_counters(self._h, out)
+        return list(out)
+
     def stats(self) -> dict:
         st, rj, rays = C.c_uint64(), C.c_uint64(), C.c_uint64()
         ln = C.c_int32()

@@ -42,6 +42,17 @@ def main():
     v.set_spheres([])
     v.s.disk_enabled = 0
     variants["sky_only"] = v
+    for n in (1, 8, 32):
+        v = base.clone()
+        v.set_spheres(base.spheres[:n])
+        variants[f"spheres_{n}"] = v
+    v = base.clone()  # one sphere far outside every ray's plane pencil
+    far = scenes.Sphere()
+    for i, x in enumerate((0.0, 90.0, 0.0)):
+        far.center[i] = x
+    far.radius = 0.5
+    v.set_spheres([far])
+    variants["sphere_far"] = v
     for name, sb in variants.items():
         ms, spr = timeit(sb)
         rays = sb.s.width * sb.s.height * sb.s.spp
