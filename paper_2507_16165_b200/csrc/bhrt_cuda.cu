@@ -447,6 +447,12 @@ int bhrt_ctx_set_scene(bhrt_ctx* c, const bhrt_scene* s, bhrt_status_info* info)
     k.sky_kind = s->sky_kind;
     k.checker_nu = s->checker_nu;
     k.checker_nv = s->checker_nv;
+    for (int i = 0; i < kCheckerMax; ++i) {  // checker cell boundaries (shade_sample)
+        const double th = -kPi + 2.0 * kPi * i / (s->checker_nu > 0 ? s->checker_nu : 1);
+        k.checker_uc[i] = std::cos(th);
+        k.checker_us[i] = std::sin(th);
+        k.checker_vc[i] = std::cos(kPi * i / (s->checker_nv > 0 ? s->checker_nv : 1));
+    }
     std::memcpy(k.checker_a, s->checker_color_a, sizeof k.checker_a);
     std::memcpy(k.checker_b, s->checker_color_b, sizeof k.checker_b);
     k.disk_enabled = s->disk_enabled;

@@ -14,6 +14,7 @@ constexpr int kQMin = -64;  // RKF45 controller table range
 constexpr int kQN = 96;
 constexpr int kMaxSpheres = 256;
 constexpr int kMaxCand = 16;
+constexpr int kCheckerMax = 64;  // checker cells resolved by threshold search (else atan2/asin)
 
 struct KParams {
     // black hole + termination
@@ -39,6 +40,9 @@ struct KParams {
     int32_t pad1;
     const uint8_t* sky;
     double checker_a[3], checker_b[3];
+    // cell boundaries: longitude k at atan2 = -pi + 2 pi k / nu as (cos, sin);
+    // latitude k at y = cos(pi k / nv)
+    double checker_uc[kCheckerMax], checker_us[kCheckerMax], checker_vc[kCheckerMax];
     // disk
     int32_t disk_enabled;
     int32_t n_spheres;

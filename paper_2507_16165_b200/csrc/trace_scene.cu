@@ -169,7 +169,7 @@ __device__ __forceinline__ void disk_line(const SceneSm& sm, int t, double& dlx,
 // Oracle step_events(): disk = exact phi-event on the step's Hermite
 // interpolant; spheres = first entering hit on S equal-angle sub-chords.
 // Returns true on hit; always advances the event state and next_ev.
-__device__ __noinline__ bool step_events(const KParams& p, SceneSm& sm, int t, double pa, double ua,
+__device__ BHRT_INL_EVT bool step_events(const KParams& p, SceneSm& sm, int t, double pa, double ua,
                                          double wa, double pb, double ub, double wb, double& next_ev,
                                          Hit& hit) {
     const double h = pb - pa;
@@ -373,7 +373,7 @@ __device__ __forceinline__ V3 tangent_dir(V3 e1, V3 e2, double phi, double u, do
 
 // Oracle escape_dir(): tangent at the r = escape_radius crossing of the last
 // step (Hermite + 2 Newton iterations, u' from the first integral).
-__device__ __noinline__ V3 escape_dir(const KParams& p, SceneSm& sm, int t, bool has_step, double pa,
+__device__ BHRT_INL_ESC V3 escape_dir(const KParams& p, SceneSm& sm, int t, bool has_step, double pa,
                                       double ua, double wa, double pb, double ub, double wb) {
     const V3 e1 = ld3(sm.e1, t), e2 = ld3(sm.e2, t);
     if (!has_step || !(ua > p.u_esc)) return tangent_dir(e1, e2, pb, ub, wb);
@@ -532,7 +532,11 @@ __global__ void __launch_bounds__(kBlock, BHRT_SCENE_MINB) trace_scene_kernel(co
                     }
                 }
             }
+#ifdef BHRT_EXPERIMENT_NOESCAPE
+            if (H.obj == BHRT_OBJ_SKY) H.point = mk(pp, up, wp);  // timing experiment only
+#else
             if (H.obj == BHRT_OBJ_SKY) H.point = escape_dir(p, sm, t, has_step, pp, up, wp, phi, u, w);
+#endif
         }
     }
     finish_sample(p, valid, id, H.obj, H.sphere, H.point, phi, nsteps, nrej);
