@@ -12,6 +12,9 @@ namespace bhrt_b200 {
 
 constexpr int kQMin = -64;  // RKF45 controller table range
 constexpr int kQN = 96;
+// Largest q with grow factor 0.9 * 2^(-(q+1)/20) >= 1 (checked against the
+// host table by tests/test_abi.py): q + 1 <= -20 log2(1/0.9) = -3.04.
+constexpr int kQGrowOne = -5;
 constexpr int kMaxSpheres = 256;
 constexpr int kMaxCand = 16;
 constexpr int kCheckerMax = 64;  // checker cells resolved by threshold search (else atan2/asin)

@@ -138,6 +138,9 @@ def test_rkf45_step_accuracy_and_controller():
     assert np.all(np.diff(g) <= 0) and g.max() == 5.0 and g.min() >= 0.2
     sh = np.array(list(shrink))
     assert sh.max() == 0.9 and sh.min() >= 0.1
+    # kernel fast path (bhrt_kernel_params.h kQGrowOne = -5): grow >= 1 exactly for q <= -5
+    qmin_ = qmin.value
+    assert g[-5 - qmin_] >= 1.0 and g[-4 - qmin_] < 1.0
     rng = np.random.default_rng(3)
     for _ in range(200):
         u, w, h = rng.uniform(0.01, 0.3), rng.uniform(-0.3, 0.3), rng.uniform(1e-3, 0.1)
