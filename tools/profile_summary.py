@@ -68,11 +68,10 @@ def full(path, label=""):
         for k in KEYS:
             if k in d:
                 print(f"| {k} | {d[k]} | {u.get(k, '')} |")
+        scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}
         try:
-            rb = float(d["dram__bytes_read.sum"]) * (1e9 if u["dram__bytes_read.sum"] == "Gbyte" else
-                                                   1e6 if u["dram__bytes_read.sum"] == "Mbyte" else 1)
-            wb = float(d["dram__bytes_write.sum"]) * (1e9 if u["dram__bytes_write.sum"] == "Gbyte" else
-                                                    1e6 if u["dram__bytes_write.sum"] == "Mbyte" else 1)
+            rb = float(d["dram__bytes_read.sum"]) * scale.get(u["dram__bytes_read.sum"], 1.0)
+            wb = float(d["dram__bytes_write.sum"]) * scale.get(u["dram__bytes_write.sum"], 1.0)
             print(f"\nDRAM traffic per launch: {rb + wb:.4g} bytes (read {rb:.4g}, write {wb:.4g})\n")
         except (KeyError, ValueError):
             pass
