@@ -142,6 +142,10 @@ __device__ double events_setup(const KParams& p, SceneSm& sm, int t, V3 e1, V3 e
         }
     }
     if (nc < 0) next_sph = -CUDART_INF_F;
+#ifdef BHRT_EXPERIMENT_NOSPHEREEVENTS
+    nc = 0;  // timing experiment only: candidates computed, never tested
+    next_sph = CUDART_INF_F;
+#endif
 #ifdef BHRT_COUNTERS
     atomicAdd(&p.stats[6], (unsigned long long)(nc < 0 ? 100 : nc));
 #endif
