@@ -104,8 +104,8 @@ __device__ double events_setup(const KParams& p, SceneSm& sm, int t, V3 e1, V3 e
         sm.lo[nc][t] = lo;
         sm.hi[nc][t] = hi;
         const float rc = sqrtf((float)(cx * cx + cy * cy)), rho = sqrtf((float)rho2);
-        sm.rlo[nc][t] = (rc - rho) * 0.999f - 1e-3f;
-        sm.rhi[nc][t] = (rc + rho) * 1.001f + 1e-3f;
+        sm.rlo[nc][t] = (rc - rho) - 1e-5f * (rc + rho);  // fp32 rounding << 1e-5
+        sm.rhi[nc][t] = (rc + rho) * (1.0f + 1e-5f);
         sm.k[nc][t] = (unsigned char)k;
         next_sph = fminf(next_sph, lo);
         ++nc;
@@ -207,14 +207,44 @@ __device__ BHRT_INL_EVT bool step_events(const KParams& p, SceneSm& sm, int t, d
     unsigned act = 0;
     if (!test_all) {
         const float fa = (float)pa, fb = (float)pb;
-        // conservative radial extent of the step's polyline: monotone u (same
-        // sign of u' at both ends) keeps it within the end radii, widened 2%
-        // for chord sagitta (h <= 0.1 rad) and interpolant overshoot
-        const float ra = 1.0f / (float)ua, rb = 1.0f / (float)ub;
+        // Conservative radial extent of the step's polyline. Its vertices lie
+        // on the Hermite interpolant u(t), t in [0, 1], whose range is spanned
+        // by the end values and the interior roots of u'(t) (fp32, widened by
+        // 1e-5 of the coefficient scale). A sub-chord of angle dl between
+        // radii r1, r2 stays within [min(r1, r2) cos(dl), max(r1, r2)].
         float slo = 0.0f, shi = CUDART_INF_F;
-        if ((wa > 0.0) == (wb > 0.0) && h <= 0.1) {
-            slo = fminf(ra, rb) * 0.98f;
-            shi = fmaxf(ra, rb) * 1.02f;
+        {
+            const float a1 = (float)cu.a1, a2 = (float)cu.a2, a3 = (float)cu.a3, a0 = (float)ua;
+            float umin = fminf(a0, (float)ub), umax = fmaxf(a0, (float)ub);
+            const float A = 3.0f * a3, B = 2.0f * a2;
+            const float disc = B * B - 4.0f * A * a1;
+            if (disc >= 0.0f && A != 0.0f) {
+                const float sq = sqrtf(disc);
+                const float ta = (-B - sq) / (2.0f * A), tb = (-B + sq) / (2.0f * A);
+                if (ta > 0.0f && ta < 1.0f) {
+                    const float v = fmaf(fmaf(fmaf(a3, ta, a2), ta, a1), ta, a0);
+                    umin = fminf(umin, v);
+                    umax = fmaxf(umax, v);
+                }
+                if (tb > 0.0f && tb < 1.0f) {
+                    const float v = fmaf(fmaf(fmaf(a3, tb, a2), tb, a1), tb, a0);
+                    umin = fminf(umin, v);
+                    umax = fmaxf(umax, v);
+                }
+            } else if (A == 0.0f && B != 0.0f) {
+                const float ta = -a1 / B;
+                if (ta > 0.0f && ta < 1.0f) {
+                    const float v = fmaf(fmaf(a2, ta, a1), ta, a0);
+                    umin = fminf(umin, v);
+                    umax = fmaxf(umax, v);
+                }
+            }
+            const float slack = 1e-5f * (fabsf(a0) + fabsf(a1) + fabsf(a2) + fabsf(a3));
+            umin -= slack;
+            umax += slack;
+            const float dl = fminf((float)h, (float)p.chord_dphi);
+            if (umax > 0.0f) slo = (1.0f / umax) * (1.0f - 0.5f * dl * dl) * (1.0f - 1e-5f);
+            if (umin > 0.0f) shi = (1.0f / umin) * (1.0f + 1e-5f);
         }
         for (int i = 0; i < nc; ++i)
             if (sm.lo[i][t] <= fb && sm.hi[i][t] >= fa && sm.rlo[i][t] <= shi && sm.rhi[i][t] >= slo)
