@@ -353,31 +353,41 @@ __device__ __forceinline__ void finish_sample(const KParams& p, bool valid, cons
 }
 
 // ================================================================= RK4 / RKF45 scene modes
+// Fehlberg tableau. Entries that are short fp64 immediates (low word zero)
+// stay literal; the rest live in constant bank 3, which DFMA reads as an
+// operand — as literals each would be rematerialised with two UMOVs per use
+// inside the step loop (128-register cap). Same double values either way.
 #define F21 (1.0 / 4.0)
 #define F31 (3.0 / 32.0)
 #define F32 (9.0 / 32.0)
-#define F41 (1932.0 / 2197.0)
-#define F42 (-7200.0 / 2197.0)
-#define F43 (7296.0 / 2197.0)
-#define F51 (439.0 / 216.0)
 #define F52 (-8.0)
-#define F53 (3680.0 / 513.0)
-#define F54 (-845.0 / 4104.0)
-#define F61 (-8.0 / 27.0)
 #define F62 (2.0)
-#define F63 (-3544.0 / 2565.0)
-#define F64 (1859.0 / 4104.0)
-#define F65 (-11.0 / 40.0)
-#define G1 (16.0 / 135.0)
-#define G3 (6656.0 / 12825.0)
-#define G4 (28561.0 / 56430.0)
-#define G5 (-9.0 / 50.0)
-#define G6 (2.0 / 55.0)
-#define H1 (1.0 / 360.0)
-#define H3 (-128.0 / 4275.0)
-#define H4 (-2197.0 / 75240.0)
-#define H5 (1.0 / 50.0)
-#define H6 (2.0 / 55.0)
+static __constant__ double kRkf[20] = {
+    1932.0 / 2197.0, -7200.0 / 2197.0, 7296.0 / 2197.0,                       // F41 F42 F43
+    439.0 / 216.0, 3680.0 / 513.0, -845.0 / 4104.0,                           // F51 F53 F54
+    -8.0 / 27.0, -3544.0 / 2565.0, 1859.0 / 4104.0, -11.0 / 40.0,             // F61 F63 F64 F65
+    16.0 / 135.0, 6656.0 / 12825.0, 28561.0 / 56430.0, -9.0 / 50.0, 2.0 / 55.0,  // G1 G3 G4 G5 G6
+    1.0 / 360.0, -128.0 / 4275.0, -2197.0 / 75240.0, 1.0 / 50.0, 2.0 / 55.0};    // H1 H3 H4 H5 H6
+#define F41 (kRkf[0])
+#define F42 (kRkf[1])
+#define F43 (kRkf[2])
+#define F51 (kRkf[3])
+#define F53 (kRkf[4])
+#define F54 (kRkf[5])
+#define F61 (kRkf[6])
+#define F63 (kRkf[7])
+#define F64 (kRkf[8])
+#define F65 (kRkf[9])
+#define G1 (kRkf[10])
+#define G3 (kRkf[11])
+#define G4 (kRkf[12])
+#define G5 (kRkf[13])
+#define G6 (kRkf[14])
+#define H1 (kRkf[15])
+#define H3 (kRkf[16])
+#define H4 (kRkf[17])
+#define H5 (kRkf[18])
+#define H6 (kRkf[19])
 
 __device__ __forceinline__ double g_of(double U, double M3) { return U * fma(M3, U, -1.0); }
 

@@ -548,10 +548,14 @@ __global__ void __launch_bounds__(kBlock, BHRT_SCENE_MINB) trace_scene_kernel(co
                             phi = pn;
                             break;
                         }
-                        pp = phi;
-                        up = u;
-                        wp = w;
-                        has_step = true;
+                        // escape_dir needs the last step only when the ray ends on the sky,
+                        // i.e. after a step that ends at u <= u_esc: save just those
+                        if (un <= p.u_esc) {
+                            pp = phi;
+                            up = u;
+                            wp = w;
+                            has_step = true;
+                        }
                         phi = pn;
                         u = un;
                         w = wn;
