@@ -112,3 +112,32 @@ def test_render_without_device_fails_loudly():
                                             out.ctypes.data_as(C.POINTER(C.c_uint8)), out.nbytes,
                                             None, C.byref(info))
     assert rc == 5  # BHRT_DEVICE: no silent CPU fallback
+
+
+def test_cull_atan2_polynomial_error_bound():
+    """trace_scene.cu atan2_cull (window / cull-bin angles only): the odd
+    minimax polynomial in the source stays within 2e-6 rad of atan2 over all
+    octants in fp32, far inside the 5e-4 rad window margin."""
+    src = open(os.path.join(ROOT, "paper_2507_16165_b200", "csrc", "trace_scene.cu")).read()
+    body = src[src.index("float atan2_cull"):]
+    body = body[:body.index("return copysignf")]
+    coef = [np.float32(c) for c in re.findall(r"(-?0\.\d+)f", body)]
+    assert len(coef) >= 6
+    c = coef[:6]  # innermost first, as written in the Horner chain
+    rng = np.random.default_rng(7)
+    ang = rng.uniform(-np.pi, np.pi, 400000)
+    rad = rng.uniform(1e-3, 1e3, ang.size)
+    y = (rad * np.sin(ang)).astype(np.float32)
+    x = (rad * np.cos(ang)).astype(np.float32)
+    ax, ay = np.abs(x), np.abs(y)
+    a = (np.minimum(ax, ay) / np.maximum(ax, ay)).astype(np.float32)
+    s = (a * a).astype(np.float32)
+    r = np.full_like(s, c[0])
+    for k in c[1:]:
+        r = (r * s + k).astype(np.float32)
+    r = (r * a).astype(np.float32)
+    r = np.where(ay > ax, np.float32(1.57079637) - r, r)
+    r = np.where(x < 0, np.float32(3.14159274) - r, r)
+    r = np.copysign(r, y)
+    err = np.abs(r.astype(np.float64) - np.arctan2(y.astype(np.float64), x.astype(np.float64)))
+    assert err.max() < 2e-6
