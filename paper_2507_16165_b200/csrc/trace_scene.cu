@@ -16,7 +16,9 @@ constexpr int kSlots = 8;
 constexpr int kSphSm = 128;          // spheres staged in shared memory
 constexpr float kWinMargin = 5e-4f;  // fp32 window slack (rad); windows only cull
 #ifndef BHRT_SCENE_MINB
-#define BHRT_SCENE_MINB 4  // min resident blocks per SM (register cap), tuned on B200
+// min resident blocks per SM (register cap 102): measured on B200, config 2:
+// 3 -> 10.3, 4 -> 8.83, 5 -> 8.65, 6 -> 9.12 ms (5 spills only outside the step)
+#define BHRT_SCENE_MINB 5
 #endif
 
 struct SceneSm {
@@ -186,6 +188,106 @@ __device__ __forceinline__ void disk_line(const SceneSm& sm, int t, double& dlx,
     Lw = dvd(L, nl);
 }
 
+// Sphere half of step_events(): first entering hit on the step's S
+// equal-angle sub-chords among the candidates in act (all spheres when the
+// candidate slots overflowed). Rare after radial culling (~0.04 per ray on
+// config 2), so it is kept out of line: its registers do not count against
+// the step loop's occupancy.
+__device__ BHRT_INL_SPH bool sphere_search(const KParams& p, const SceneSm& sm, int t, double pa, double h,
+                                           double ua, double ub, const Cubic cu, unsigned act, int nc,
+                                           int& bsph, double& bqx, double& bqy) {
+    const bool test_all = nc < 0;
+    // Candidate-outer evaluation of the oracle's sub-chord-outer search:
+    // each candidate scans only the sub-chords its (conservative) window
+    // overlaps and stops at its first hit; the winner is the
+    // lexicographic minimum of (sub-chord, chord parameter), ties to the
+    // lower slot — the same hit the oracle finds.
+    int S = 1;
+    if (h > p.chord_dphi) S = (int)ceil(h / p.chord_dphi);
+    const double dl = h / S;
+    double cd_, sd_, c0, s0;
+    if (dl <= 0.02) {
+        // sub-chord rotation: Taylor series, truncation < 1e-20 for dl <= 0.02
+        // (the oracle calls cos/sin; both are correctly rounded to ~1 ulp)
+        const double d2 = dl * dl;
+        cd_ = fma(fma(fma(fma(d2, -1.0 / 3628800.0, 1.0 / 40320.0), d2, -1.0 / 720.0), d2, 1.0 / 24.0),
+                  d2 * d2, fma(d2, -0.5, 1.0));
+        sd_ = fma(fma(fma(fma(d2, 1.0 / 362880.0, -1.0 / 5040.0), d2, 1.0 / 120.0), d2, -1.0 / 6.0),
+                  d2 * dl, dl);
+    } else {
+        sincos(dl, &sd_, &cd_);
+    }
+    sincos(pa, &s0, &c0);
+    const float fpa = (float)pa, rdl = 1.0f / (float)dl;  // conservative range only
+    int best_j = S;
+    double best_t = CUDART_INF;
+    const int ncand = test_all ? p.n_spheres : nc;
+    for (int a = 0; a < ncand; ++a) {
+        int k, j0 = 0, j1 = S - 1;
+        if (test_all) {
+            k = a;
+        } else {
+            if (!(act & (1u << a))) continue;
+            k = sm.k[a][t];
+            // clamp in float first: windows may be infinite
+            const float fS = (float)S;
+            j0 = (int)fminf(fmaxf(floorf((sm.lo[a][t] - fpa) * rdl) - 1.0f, 0.0f), fS);
+            j1 = (int)fminf(fmaxf(floorf((sm.hi[a][t] - fpa) * rdl) + 1.0f, 0.0f), fS - 1.0f);
+        }
+        j1 = min(j1, best_j);
+        if (j0 > j1) continue;
+        const V3 e1 = ld3(sm.e1, t), e2 = ld3(sm.e2, t), n = ld3(sm.n, t);
+        const V3 c = sphere_c(p, k);
+        const double r = __ldg(&p.spheres[k].radius);
+        const double dn = dot(c, n);
+        if (!(fabs(dn) < r)) continue;
+        const double ccx = dot(c, e1), ccy = dot(c, e2);  // = the oracle's cand_t values
+        const double rho2 = r * r - dn * dn;
+        double cj = c0, sj = s0;
+        for (int j = 0; j < j0; ++j) {  // same recurrence values as the sequential walk
+            const double ck = cj * cd_ - sj * sd_;
+            sj = sj * cd_ + cj * sd_;
+            cj = ck;
+        }
+        const double uj = j0 == 0 ? ua : hermite_eval(cu, (double)j0 / S);
+        const double rj = 1.0 / uj;
+        double xj = cj * rj, yj = sj * rj;
+        for (int j = j0; j <= j1; ++j) {
+            const double ck = cj * cd_ - sj * sd_;
+            const double sk = sj * cd_ + cj * sd_;
+            const double uk = (j + 1 == S) ? ub : hermite_eval(cu, (double)(j + 1) / S);
+            const double rk = 1.0 / uk;
+            const double xk = ck * rk, yk = sk * rk;
+            const double dx = xk - xj, dy = yk - yj;
+            const double mx = xj - ccx, my = yj - ccy;
+            const double A = dx * dx + dy * dy;
+            const double Bq = mx * dx + my * dy;
+            const double Cq = mx * mx + my * my - rho2;
+            if (Cq > 0.0) {
+                const double disc = Bq * Bq - A * Cq;
+                if (!(disc < 0.0)) {
+                    const double tq = (-Bq - sqrt(disc)) / A;
+                    if (tq >= 0.0 && tq <= 1.0) {
+                        if (j < best_j || tq < best_t) {
+                            best_j = j;
+                            best_t = tq;
+                            bsph = k;
+                            bqx = xj + tq * dx;
+                            bqy = yj + tq * dy;
+                        }
+                        break;
+                    }
+                }
+            }
+            cj = ck;
+            sj = sk;
+            xj = xk;
+            yj = yk;
+        }
+    }
+    return best_j < S;
+}
+
 // Oracle step_events(): disk = exact phi-event on the step's Hermite
 // interpolant; spheres = first entering hit on S equal-angle sub-chords.
 // Returns true on hit; always advances the event state and next_ev.
@@ -270,95 +372,7 @@ __device__ BHRT_INL_EVT bool step_events(const KParams& p, SceneSm& sm, int t, d
     int bsph = -1;
     double bqx = 0.0, bqy = 0.0;
     if (act || test_all) {
-        // Candidate-outer evaluation of the oracle's sub-chord-outer search:
-        // each candidate scans only the sub-chords its (conservative) window
-        // overlaps and stops at its first hit; the winner is the
-        // lexicographic minimum of (sub-chord, chord parameter), ties to the
-        // lower slot — the same hit the oracle finds.
-        int S = 1;
-        if (h > p.chord_dphi) S = (int)ceil(h / p.chord_dphi);
-        const double dl = h / S;
-        double cd_, sd_, c0, s0;
-        if (dl <= 0.02) {
-            // sub-chord rotation: Taylor series, truncation < 1e-20 for dl <= 0.02
-            // (the oracle calls cos/sin; both are correctly rounded to ~1 ulp)
-            const double d2 = dl * dl;
-            cd_ = fma(fma(fma(fma(d2, -1.0 / 3628800.0, 1.0 / 40320.0), d2, -1.0 / 720.0), d2, 1.0 / 24.0),
-                      d2 * d2, fma(d2, -0.5, 1.0));
-            sd_ = fma(fma(fma(fma(d2, 1.0 / 362880.0, -1.0 / 5040.0), d2, 1.0 / 120.0), d2, -1.0 / 6.0),
-                      d2 * dl, dl);
-        } else {
-            sincos(dl, &sd_, &cd_);
-        }
-        sincos(pa, &s0, &c0);
-        const float fpa = (float)pa, rdl = 1.0f / (float)dl;  // conservative range only
-        int best_j = S;
-        double best_t = CUDART_INF;
-        const int ncand = test_all ? p.n_spheres : nc;
-        for (int a = 0; a < ncand; ++a) {
-            int k, j0 = 0, j1 = S - 1;
-            if (test_all) {
-                k = a;
-            } else {
-                if (!(act & (1u << a))) continue;
-                k = sm.k[a][t];
-                // clamp in float first: windows may be infinite
-                const float fS = (float)S;
-                j0 = (int)fminf(fmaxf(floorf((sm.lo[a][t] - fpa) * rdl) - 1.0f, 0.0f), fS);
-                j1 = (int)fminf(fmaxf(floorf((sm.hi[a][t] - fpa) * rdl) + 1.0f, 0.0f), fS - 1.0f);
-            }
-            j1 = min(j1, best_j);
-            if (j0 > j1) continue;
-            const V3 e1 = ld3(sm.e1, t), e2 = ld3(sm.e2, t), n = ld3(sm.n, t);
-            const V3 c = sphere_c(p, k);
-            const double r = __ldg(&p.spheres[k].radius);
-            const double dn = dot(c, n);
-            if (!(fabs(dn) < r)) continue;
-            const double ccx = dot(c, e1), ccy = dot(c, e2);  // = the oracle's cand_t values
-            const double rho2 = r * r - dn * dn;
-            double cj = c0, sj = s0;
-            for (int j = 0; j < j0; ++j) {  // same recurrence values as the sequential walk
-                const double ck = cj * cd_ - sj * sd_;
-                sj = sj * cd_ + cj * sd_;
-                cj = ck;
-            }
-            const double uj = j0 == 0 ? ua : hermite_eval(cu, (double)j0 / S);
-            const double rj = 1.0 / uj;
-            double xj = cj * rj, yj = sj * rj;
-            for (int j = j0; j <= j1; ++j) {
-                const double ck = cj * cd_ - sj * sd_;
-                const double sk = sj * cd_ + cj * sd_;
-                const double uk = (j + 1 == S) ? ub : hermite_eval(cu, (double)(j + 1) / S);
-                const double rk = 1.0 / uk;
-                const double xk = ck * rk, yk = sk * rk;
-                const double dx = xk - xj, dy = yk - yj;
-                const double mx = xj - ccx, my = yj - ccy;
-                const double A = dx * dx + dy * dy;
-                const double Bq = mx * dx + my * dy;
-                const double Cq = mx * mx + my * my - rho2;
-                if (Cq > 0.0) {
-                    const double disc = Bq * Bq - A * Cq;
-                    if (!(disc < 0.0)) {
-                        const double tq = (-Bq - sqrt(disc)) / A;
-                        if (tq >= 0.0 && tq <= 1.0) {
-                            if (j < best_j || tq < best_t) {
-                                best_j = j;
-                                best_t = tq;
-                                bsph = k;
-                                bqx = xj + tq * dx;
-                                bqy = yj + tq * dy;
-                            }
-                            break;
-                        }
-                    }
-                }
-                cj = ck;
-                sj = sk;
-                xj = xk;
-                yj = yk;
-            }
-        }
-        sph_hit = best_j < S;
+        sph_hit = sphere_search(p, sm, t, pa, h, ua, ub, cu, act, nc, bsph, bqx, bqy);
         if (sph_hit) {
             const V3 e1 = ld3(sm.e1, t), e2 = ld3(sm.e2, t);
             hit.point = add(vld(p.center), add(scl(e1, bqx), scl(e2, bqy)));
