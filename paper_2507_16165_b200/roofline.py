@@ -11,9 +11,10 @@ per step attempt (accepted or rejected):
   RK4        39  = 4 rhs x 3 + stage inputs 12 + combination 14 + phi 1
   REFERENCE 152  = DOPRI5 step incl. error norm and PI control
 per ray (scene modes): camera ray 31 + plane basis 38 + initial
-  conditions 33 + plane normal 9 + disk line 16 + sphere cull 5/sphere.
-Event (polyline hit-test) and shading arithmetic are not counted, so the
-achieved figure is a lower bound.
+  conditions 33 + plane normal 9 + disk line 16. Sphere candidate tests are
+not counted (the kernel's plane-angle cull table skips most of the oracle's
+per-sphere |c.n| < r tests), nor are event (polyline hit-test) and shading
+arithmetic, so the achieved figure is a lower bound.
 """
 from __future__ import annotations
 
@@ -26,7 +27,7 @@ def setup_flops(scene) -> float:
     s = scene.s if hasattr(scene, "s") else scene
     if s.integrator == INTEGRATOR_REFERENCE:
         return 31.0 + 38.0 + 33.0
-    return 31.0 + 38.0 + 33.0 + 9.0 + (16.0 if s.disk_enabled else 0.0) + 5.0 * s.n_spheres
+    return 31.0 + 38.0 + 33.0 + 9.0 + (16.0 if s.disk_enabled else 0.0)
 
 
 def launch_flops(scene, stats: dict) -> float:
