@@ -187,6 +187,25 @@ int bhrt_cuda_render_rows(const bhrt_scene* scene, int32_t row_start, int32_t ro
                           const int32_t* devices, int32_t ndev, uint8_t* out, size_t out_len,
                           bhrt_ray_record* records, bhrt_status_info* info);
 
+/* Batch form of the reference's per-ray entry points:
+ * trace() (geodesic.hpp:107-108, geodesic.cpp:164-238) and, when
+ * `deflection` is not NULL, deflection_of_ray() (geodesic.hpp:110-113,
+ * geodesic.cpp:240-262), for n caller rays. rays = n x {origin[3], dir[3]}
+ * (host, row-major). Uses the scene's mass, center, epsilon, escape_radius,
+ * max_windings, rel_tol, abs_tol; camera, samples and sky are ignored; the
+ * integrator must be BHRT_INTEGRATOR_REFERENCE. Outcomes instead of
+ * polylines: records[i].object = HORIZON (Captured) / SKY (Escaped; point =
+ * unit escape direction, the normalised last chord) / STALLED, or
+ * -BHRT_NUMERICAL; steps/rejected = DOPRI5 steps; phi = final phi.
+ * deflection[i] = |total turning| for escaped rays, NaN otherwise (the
+ * reference throws NumericalError there). Errors as the reference's: trace
+ * config or mass invalid -> BHRT_INVALID_ARGUMENT; an origin inside the
+ * horizon -> BHRT_INVALID_ARGUMENT with info->px = lowest such ray index;
+ * numerical failures -> BHRT_NUMERICAL with info->px = lowest failing ray
+ * (records are filled for every ray). device < 0: the current device. */
+int bhrt_cuda_trace_rays(const bhrt_scene* scene, const double* rays, int64_t n, int32_t device,
+                         bhrt_ray_record* records, double* deflection, bhrt_status_info* info);
+
 /* ---- persistent context: scene resident in HBM, async launches ---- */
 typedef struct bhrt_ctx bhrt_ctx;
 

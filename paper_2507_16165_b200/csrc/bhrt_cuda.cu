@@ -23,6 +23,8 @@ namespace bhrt_b200 {
 int launch_trace(const KParams& p, cudaStream_t st, int* launches, cudaEvent_t* ev);
 void launch_table_build(const KParams& p, double* smp, double* ends, int32_t* kind, int32_t* n, cudaStream_t st);
 void launch_table_bind(const KParams& p, double* ends, double* psi0, double u0, cudaStream_t st);
+void launch_trace_rays(const KParams& p, const double* rays, long long n, bhrt_ray_record* records,
+                       double* defl, cudaStream_t st);
 
 namespace {
 
@@ -192,6 +194,7 @@ struct bhrt_ctx {
     DevBuf<bhrt_sphere> spheres;
     DevBuf<double> tables;
     DevBuf<bhrt_ray_record> records;
+    DevBuf<double> rays, defl;  // bhrt_cuda_trace_rays
     DevBuf<uint8_t> out;
     DevBuf<unsigned long long> stats;
     DevBuf<unsigned int> queue;
@@ -714,5 +717,68 @@ extern "C" int bhrt_cuda_render_rows(const bhrt_scene* s, int32_t row_start, int
             }
         }
     }
+    return 0;
+}
+
+// trace() / deflection_of_ray() for a batch of caller rays.
+extern "C" int bhrt_cuda_trace_rays(const bhrt_scene* s, const double* rays, int64_t n, int32_t device,
+                                    bhrt_ray_record* records, double* deflection,
+                                    bhrt_status_info* info) {
+    if (!s || n < 0 || (n > 0 && (!rays || !records)))
+        return set_info(info, BHRT_INVALID_ARGUMENT, -1, -1, "trace_rays: bad arguments");
+    // trace(): validate(cfg) (geodesic.cpp:19-27) then the mass (:167)
+    if (!(s->epsilon > 0.0))
+        return set_info(info, BHRT_INVALID_ARGUMENT, -1, -1, "trace config: epsilon must be > 0");
+    if (!(s->escape_radius > 0.0))
+        return set_info(info, BHRT_INVALID_ARGUMENT, -1, -1, "trace config: escape_radius must be > 0");
+    if (s->max_windings < 1)
+        return set_info(info, BHRT_INVALID_ARGUMENT, -1, -1, "trace config: max_windings must be >= 1");
+    if (!(s->rel_tol > 0.0))
+        return set_info(info, BHRT_INVALID_ARGUMENT, -1, -1, "trace config: rel_tol must be > 0");
+    if (!(s->abs_tol > 0.0))
+        return set_info(info, BHRT_INVALID_ARGUMENT, -1, -1, "trace config: abs_tol must be > 0");
+    if (s->mass < 0.0) return set_info(info, BHRT_INVALID_ARGUMENT, -1, -1, "trace: mass must be >= 0");
+    if (s->integrator != BHRT_INTEGRATOR_REFERENCE)
+        return set_info(info, BHRT_INVALID_ARGUMENT, -1, -1, "trace_rays: integrator must be REFERENCE");
+    for (int64_t i = 0; i < n; ++i) {  // geodesic.cpp:169-172
+        const HV3 v = hsub(hv(rays + 6 * i), hv(s->center));
+        if (s->mass > 0.0 && hnorm(v) <= 2.0 * s->mass)
+            return set_info(info, BHRT_INVALID_ARGUMENT, static_cast<int>(i), -1,
+                            "trace: ray origin is not outside the event horizon");
+    }
+    if (n == 0) return 0;
+    std::lock_guard<std::mutex> lock(g_ctx_mu);
+    int dev = device;
+    if (dev < 0) CK(cudaGetDevice(&dev));
+    bhrt_ctx* c = nullptr;
+    int rc = cached_ctx(dev, &c, info);
+    if (rc) return rc;
+    CK(cudaSetDevice(dev));
+    if (c->rays.ensure(6 * static_cast<size_t>(n)) || c->records.ensure(static_cast<size_t>(n)) ||
+        (deflection && c->defl.ensure(static_cast<size_t>(n))))
+        return set_info(info, BHRT_DEVICE, -1, -1, "trace_rays: alloc failed");
+    KParams k;
+    std::memset(&k, 0, sizeof k);
+    k.mass = s->mass;
+    k.M3 = 3.0 * s->mass;
+    std::memcpy(k.center, s->center, sizeof k.center);
+    k.u_cap = s->mass > 0.0 ? 1.0 / (2.0 * s->mass) : INFINITY;
+    k.u_esc = 1.0 / s->escape_radius;
+    k.escape_radius = s->escape_radius;
+    k.phi_max = 2.0 * kPi * s->max_windings;
+    k.max_windings = s->max_windings;
+    k.integrator = s->integrator;
+    k.epsilon = s->epsilon;
+    k.rel_tol = s->rel_tol;
+    k.abs_tol = s->abs_tol;
+    CK(cudaMemcpy(c->rays.p, rays, sizeof(double) * 6 * n, cudaMemcpyHostToDevice));
+    launch_trace_rays(k, c->rays.p, n, c->records.p, deflection ? c->defl.p : nullptr, nullptr);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(records, c->records.p, sizeof(bhrt_ray_record) * n, cudaMemcpyDeviceToHost));
+    if (deflection) CK(cudaMemcpy(deflection, c->defl.p, sizeof(double) * n, cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < n; ++i)
+        if (records[i].object == -BHRT_NUMERICAL)
+            return set_info(info, BHRT_NUMERICAL, static_cast<int>(i), -1,
+                            "trace: inverse radius left the positive domain or step underflow");
     return 0;
 }

@@ -114,6 +114,73 @@ __device__ __forceinline__ V3 plane_point(V3 origin, V3 e1, V3 e2, double r, dou
     return add(origin, scl(add(scl(e1, cos(phi)), scl(e2, sin(phi))), r));
 }
 
+struct RResult {
+    int obj;        // HORIZON / SKY / STALLED or -BHRT_NUMERICAL
+    V3 edir;        // escape direction (SKY with at least one window)
+    bool chord;     // edir is valid (else the ray escapes along its launch direction)
+    double phi;     // phi at termination
+    double defl;    // deflection_of_ray total (DEFL only)
+};
+
+// trace() window loop, geodesic.cpp:189-236, for a non-radial ray with
+// orbital-plane basis (e1, e2) and initial state (u, w). Only (phi, u) of the
+// last two window ends are kept; the escape direction is the normalised last
+// chord of the polyline (geodesic.cpp:211-212). With DEFL the per-segment
+// turning of deflection_of_ray (geodesic.cpp:248-260) is accumulated too.
+template <bool DEFL>
+__device__ __forceinline__ RResult window_loop(const KParams& p, V3 origin, V3 center, V3 e1, V3 e2,
+                                               double u, double w, unsigned& nsteps, unsigned& nrej) {
+    RResult R;
+    R.obj = BHRT_OBJ_NONE;
+    R.edir = mk(0.0, 0.0, 0.0);
+    R.chord = false;
+    R.defl = 0.0;
+    double phi = 0.0, hint = 0.0;
+    double prev_phi = 0.0, prev_u = 0.0, last_phi = 0.0, last_u = 0.0;
+    int npts = 1;
+    V3 p_prev = origin;
+    double prev_x = 0.0, prev_y = 0.0;
+    for (;;) {
+        if (u >= p.u_cap) { R.obj = BHRT_OBJ_HORIZON; break; }
+        if (u <= p.u_esc && w < 0.0) {
+            R.obj = BHRT_OBJ_SKY;
+            if (npts >= 2) {
+                const V3 last = plane_point(center, e1, e2, 1.0 / last_u, last_phi);
+                const V3 prev = npts == 2 ? origin : plane_point(center, e1, e2, 1.0 / prev_u, prev_phi);
+                R.edir = normalized(sub(last, prev));
+                R.chord = true;
+            }
+            break;
+        }
+        if (phi > p.phi_max) { R.obj = BHRT_OBJ_STALLED; break; }
+        // segment_dphi, geodesic.cpp:76-80
+        const double hyp = glibc_hypot(u, w);
+        const double dphi = clampd(p.epsilon * u * u / hyp, 1e-6, 0.1);
+        if (!integrate_window(phi, u, w, dphi, p.mass, p.rel_tol, p.abs_tol, hint, nsteps, nrej)) {
+            if (p.mass > 0.0 && u >= p.u_cap) { R.obj = BHRT_OBJ_HORIZON; break; }
+            R.obj = -BHRT_NUMERICAL;
+            break;
+        }
+        if (!(u > 0.0)) { R.obj = -BHRT_NUMERICAL; break; }
+        prev_phi = last_phi;
+        prev_u = last_u;
+        last_phi = phi;
+        last_u = u;
+        ++npts;
+        if (DEFL) {
+            const V3 pt = plane_point(center, e1, e2, 1.0 / u, phi);
+            const V3 seg = sub(pt, p_prev);
+            const double sx = dot(seg, e1), sy = dot(seg, e2);
+            if (npts > 2) R.defl += atan2(prev_x * sy - prev_y * sx, prev_x * sx + prev_y * sy);
+            prev_x = sx;
+            prev_y = sy;
+            p_prev = pt;
+        }
+    }
+    R.phi = phi;
+    return R;
+}
+
 __global__ void __launch_bounds__(128) trace_reference_kernel(const __grid_constant__ KParams p) {
     const long long n = (long long)p.n_rows * p.width * p.spp;
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -126,52 +193,75 @@ __global__ void __launch_bounds__(128) trace_reference_kernel(const __grid_const
     if (valid) {
         const V3 origin = vld(p.cam_pos), center = vld(p.center);
         const V3 dir = camera_ray(p, id.x, id.y, id.s);
-        const V3 v = sub(origin, center);
-        const double r0 = norm(v);
         const Basis B = plane_basis(p, dir);
         edir = dir;
         if (!B.ok) {  // radial: geodesic.cpp:175-187
             obj = dot(dir, sub(center, origin)) > 0.0 ? BHRT_OBJ_HORIZON : BHRT_OBJ_SKY;
-            (void)r0;
         } else {
-            double u, w, phi = 0.0, hint = 0.0;
+            double u, w;
             initial_conditions(p, dir, u, w);
-            double prev_phi = 0.0, prev_u = 0.0, last_phi = 0.0, last_u = 0.0;
-            int npts = 1;
-            obj = BHRT_OBJ_NONE;
-            for (;;) {
-                if (u >= p.u_cap) { obj = BHRT_OBJ_HORIZON; break; }
-                if (u <= p.u_esc && w < 0.0) {
-                    obj = BHRT_OBJ_SKY;
-                    if (npts >= 2) {
-                        const V3 last = plane_point(center, B.e1, B.e2, 1.0 / last_u, last_phi);
-                        const V3 prev = npts == 2 ? origin
-                                                  : plane_point(center, B.e1, B.e2, 1.0 / prev_u, prev_phi);
-                        edir = normalized(sub(last, prev));
-                    }
-                    break;
-                }
-                if (phi > p.phi_max) { obj = BHRT_OBJ_STALLED; break; }
-                // segment_dphi, geodesic.cpp:76-80
-                const double hyp = glibc_hypot(u, w);
-                const double dphi = clampd(p.epsilon * u * u / hyp, 1e-6, 0.1);
-                if (!integrate_window(phi, u, w, dphi, p.mass, p.rel_tol, p.abs_tol, hint, nsteps, nrej)) {
-                    if (p.mass > 0.0 && u >= p.u_cap) { obj = BHRT_OBJ_HORIZON; break; }
-                    obj = -BHRT_NUMERICAL;
-                    break;
-                }
-                if (!(u > 0.0)) { obj = -BHRT_NUMERICAL; break; }
-                prev_phi = last_phi;
-                prev_u = last_u;
-                last_phi = phi;
-                last_u = u;
-                ++npts;
-            }
-            phi_end = phi;
+            const RResult R = window_loop<false>(p, origin, center, B.e1, B.e2, u, w, nsteps, nrej);
+            obj = R.obj;
+            if (obj == BHRT_OBJ_SKY && R.chord) edir = R.edir;
+            phi_end = R.phi;
         }
     }
     finish_sample(p, valid, id, obj, -1, edir, phi_end, nsteps, nrej);
     warp_add_stats(p.stats, nsteps, nrej, valid ? 1ull : 0ull);
+}
+
+// Ray batch (bhrt_cuda_trace_rays): the reference's
+// trace() (geodesic.cpp:164-238) on caller rays {origin[3], dir[3]}, one
+// record per ray; with defl != nullptr also deflection_of_ray
+// (geodesic.cpp:240-262; NaN unless the ray escapes). The per-ray basis and
+// initial state follow geodesic.cpp:49-65 (oracle orc_plane_basis /
+// orc_initial_conditions, same operations). Origins inside the horizon are
+// rejected on the host before launch.
+template <bool DEFL>
+__global__ void __launch_bounds__(128) trace_rays_kernel(const __grid_constant__ KParams p, const double* rays,
+                                                         long long n, bhrt_ray_record* records, double* defl) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const V3 origin = vld(rays + 6 * i), dir = vld(rays + 6 * i + 3), center = vld(p.center);
+    unsigned nsteps = 0, nrej = 0;
+    bhrt_ray_record rec;
+    rec.sphere = -1;
+    rec.phi = 0.0;
+    V3 pt = mk(0.0, 0.0, 0.0);
+    double d = 0.0;
+    const V3 v = sub(origin, center);
+    const V3 e1 = normalized(v);
+    const V3 tangential = sub(dir, scl(e1, dot(dir, e1)));
+    if (norm(tangential) < 1e-12) {  // radial: geodesic.cpp:175-187
+        rec.object = dot(dir, sub(center, origin)) > 0.0 ? BHRT_OBJ_HORIZON : BHRT_OBJ_SKY;
+        if (rec.object == BHRT_OBJ_SKY) pt = dir;
+    } else {
+        const V3 e2 = normalized(tangential);
+        const double r0 = norm(v);
+        const double b = norm(cross(v, dir));
+        const double u = 1.0 / r0, w = -dot(v, dir) / (r0 * b);
+        const RResult R = window_loop<DEFL>(p, origin, center, e1, e2, u, w, nsteps, nrej);
+        rec.object = R.obj;
+        if (R.obj == BHRT_OBJ_SKY) pt = R.chord ? R.edir : dir;
+        rec.phi = R.phi;
+        d = fabs(R.defl);
+    }
+    rec.steps = (int)nsteps;
+    rec.rejected = (int)nrej;
+    rec.point[0] = pt.x;
+    rec.point[1] = pt.y;
+    rec.point[2] = pt.z;
+    records[i] = rec;
+    if (DEFL) defl[i] = rec.object == BHRT_OBJ_SKY ? d : CUDART_NAN;
+}
+
+void launch_trace_rays(const KParams& p, const double* rays, long long n, bhrt_ray_record* records,
+                       double* defl, cudaStream_t st) {
+    const unsigned blocks = (unsigned)((n + 127) / 128);
+    if (defl)
+        trace_rays_kernel<true><<<blocks, 128, 0, st>>>(p, rays, n, records, defl);
+    else
+        trace_rays_kernel<false><<<blocks, 128, 0, st>>>(p, rays, n, records, nullptr);
 }
 
 void launch_reference(const KParams& p, cudaStream_t st) {

@@ -141,3 +141,23 @@ def test_cull_atan2_polynomial_error_bound():
     r = np.copysign(r, y)
     err = np.abs(r.astype(np.float64) - np.arctan2(y.astype(np.float64), x.astype(np.float64)))
     assert err.max() < 2e-6
+
+
+def test_trace_rays_host_validation_without_gpu():
+    """bhrt_cuda_trace_rays validates like the reference's trace()
+    (geodesic.cpp:19-27,166-172) before touching a device."""
+    from paper_2507_16165_b200 import geodesic as G
+    c = G.TraceConfig()
+    with pytest.raises(G.InvalidArgument, match="epsilon"):
+        G.trace_batch([(20, 0, 0)], [(0, 1, 0)], G.BlackHole(1.0), G.TraceConfig(epsilon=0.0))
+    with pytest.raises(G.InvalidArgument, match="max_windings"):
+        G.trace_batch([(20, 0, 0)], [(0, 1, 0)], G.BlackHole(1.0), G.TraceConfig(max_windings=0))
+    with pytest.raises(G.InvalidArgument, match="mass"):
+        G.trace_batch([(20, 0, 0)], [(0, 1, 0)], G.BlackHole(-1.0), c)
+    with pytest.raises(G.InvalidArgument, match="horizon") as e:
+        G.trace_batch([(20, 0, 0), (3, 0, 0), (1, 0, 0)], [(0, 1, 0)] * 3, G.BlackHole(2.0), c)
+    assert e.value.px == 1
+    rec, defl = G.trace_batch(np.zeros((0, 3)), np.zeros((0, 3)), G.BlackHole(1.0), c, deflection=True)
+    assert len(rec) == 0 and len(defl) == 0
+    with pytest.raises(G.InvalidArgument, match="deflection_angle"):
+        G.deflection_angle(0.0)
