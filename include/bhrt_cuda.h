@@ -187,6 +187,25 @@ int bhrt_cuda_render_rows(const bhrt_scene* scene, int32_t row_start, int32_t ro
                           const int32_t* devices, int32_t ndev, uint8_t* out, size_t out_len,
                           bhrt_ray_record* records, bhrt_status_info* info);
 
+/* Scene text: the reference's key=value scene format
+ * (config.hpp parse_kv / serialize_scene / parse_scene, config.cpp:27-132)
+ * extended with optional keys for the north-star features (integrator, step,
+ * max-step, chord-dphi, sky, checker, checker-color-a/b, disk, disk-color-in/
+ * out, spheres = count,seed[,shells..], sphere.<i> = cx,cy,cz,r,R,G,B,
+ * light-dir, ambient, table-*; full list in csrc/scene_text.cpp).
+ * parse: the fourteen reference keys are required, extension keys default to
+ * bhrt_scene_defaults; errors are BHRT_USAGE with the reference's messages.
+ * Spheres are written to `spheres` (capacity `cap`); *n_spheres receives the
+ * count (BHRT_INVALID_ARGUMENT when cap is too small). The background image
+ * is not part of the text (as in parse_scene): sky_rgb is left NULL.
+ * format: reference keys in serialize_scene order and number format, then
+ * only the extension keys that differ from the defaults, so a reference scene
+ * formats byte-identically to serialize_scene. *len = text length without
+ * the NUL; returns BHRT_INVALID_ARGUMENT when buf is NULL or cap <= *len. */
+int bhrt_scene_parse_text(const char* text, bhrt_scene* scene, bhrt_sphere* spheres, int32_t cap,
+                          int32_t* n_spheres, bhrt_status_info* info);
+int bhrt_scene_format_text(const bhrt_scene* scene, char* buf, size_t cap, size_t* len);
+
 /* Batch form of the reference's per-ray entry points:
  * trace() (geodesic.hpp:107-108, geodesic.cpp:164-238) and, when
  * `deflection` is not NULL, deflection_of_ray() (geodesic.hpp:110-113,

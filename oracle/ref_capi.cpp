@@ -10,6 +10,7 @@
 
 #include "bhrt/bench.hpp"
 #include "bhrt/camera.hpp"
+#include "bhrt/config.hpp"
 #include "bhrt/geodesic.hpp"
 #include "bhrt/image.hpp"
 #include "bhrt/render.hpp"
@@ -227,6 +228,39 @@ double ref_strong_scaling_mean(const bhrt_scene* s, int threads, int repeats) {
     }
     delete bg;
     return mean;
+}
+
+// config.cpp:96-112 serialize_scene of the scene's reference fields.
+// Returns the text length; writes when cap is large enough.
+size_t ref_serialize_scene(const bhrt_scene* s, char* buf, size_t cap) {
+    const std::string t = serialize_scene(to_scene(s, nullptr));
+    if (buf && cap > t.size()) std::memcpy(buf, t.c_str(), t.size() + 1);
+    return t.size();
+}
+
+// config.cpp:27-44,114-130 parse_scene(parse_kv(text)) into the reference
+// fields of `out` (other fields untouched). BHRT_USAGE + message on error.
+int ref_parse_scene(const char* text, bhrt_scene* out, bhrt_status_info* info) {
+    try {
+        const SceneConfig sc = parse_scene(parse_kv(text));
+        out->mass = sc.hole.mass;
+        put(out->center, sc.hole.center);
+        put(out->cam_pos, sc.camera.position);
+        put(out->cam_look_at, sc.camera.look_at);
+        out->vertical_fov = sc.camera.vertical_fov;
+        out->width = sc.camera.width;
+        out->height = sc.camera.height;
+        out->spp = sc.samples.spp;
+        out->seed = sc.samples.seed;
+        out->epsilon = sc.trace.epsilon;
+        out->escape_radius = sc.trace.escape_radius;
+        out->max_windings = sc.trace.max_windings;
+        out->rel_tol = sc.trace.rel_tol;
+        out->abs_tol = sc.trace.abs_tol;
+        return 0;
+    } catch (const UsageError& e) {
+        return fill(info, BHRT_USAGE, -1, -1, e.what());
+    }
 }
 
 }  // extern "C"

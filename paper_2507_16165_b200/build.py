@@ -25,7 +25,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ["-O3", "-std=c++17", "-lineinfo", "--fmad=false", "-Xptxas", "-v",
            "-Xcompiler", "-fPIC,-ffp-contract=off,-O2", "-I" + os.path.join(ROOT, "include")]
 SOURCES = ["trace_reference.cu", "trace_scene.cu", "table.cu", "shade.cu", "bhrt_cuda.cu",
-           "fp64_peak.cu"]
+           "fp64_peak.cu", "scene_text.cpp"]
 
 
 def _stale(target: str, deps: list[str]) -> bool:
@@ -42,7 +42,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
         objs = []
         os.makedirs(os.path.join(ROOT, "build"), exist_ok=True)
         for src in SOURCES:
-            obj = os.path.join(ROOT, "build", src.replace(".cu", ".o"))
+            obj = os.path.join(ROOT, "build", os.path.splitext(src)[0] + ".o")
             cmd = [NVCC, *ARCH, *NVFLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
             r = subprocess.run(cmd, capture_output=True, text=True)
             if r.returncode != 0:

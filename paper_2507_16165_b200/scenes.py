@@ -125,6 +125,42 @@ class SceneBuf:
     def spheres(self):
         return [self._spheres[i] for i in range(self.s.n_spheres)] if self.s.n_spheres else []
 
+    def to_text(self) -> str:
+        """Scene text (bhrt_scene_format_text): the reference's serialize_scene
+        keys (config.cpp:96-112) plus the extension keys that differ from the
+        defaults. The sky image is not part of the text."""
+        from . import native
+        n = C.c_size_t()
+        native.lib().bhrt_scene_format_text(self.ptr(), None, 0, C.byref(n))
+        buf = C.create_string_buffer(n.value + 1)
+        rc = native.lib().bhrt_scene_format_text(self.ptr(), buf, n.value + 1, C.byref(n))
+        if rc:
+            raise RuntimeError(f"bhrt_scene_format_text failed ({rc})")
+        return buf.value.decode()
+
+    @staticmethod
+    def from_text(text: str, sky: np.ndarray | None = None) -> "SceneBuf":
+        """Inverse of to_text (bhrt_scene_parse_text; parse_scene semantics for
+        the reference keys, config.cpp:114-130). Raises UsageError-coded
+        BhrtError on a malformed text, like the reference's UsageError."""
+        from . import native
+        from .abi import StatusInfo
+        sb = SceneBuf()
+        info = StatusInfo()
+        need = C.c_int32()
+        raw = text.encode()
+        rc = native.lib().bhrt_scene_parse_text(raw, sb.ptr(), None, 0, C.byref(need), C.byref(info))
+        if rc == 6 and need.value > 0:  # sphere buffer too small: retry with the count
+            arr = (Sphere * need.value)()
+            rc = native.lib().bhrt_scene_parse_text(raw, sb.ptr(), arr, need.value, C.byref(need),
+                                                    C.byref(info))
+            if rc == 0:
+                sb.set_spheres(list(arr))
+        native.check(rc, info)
+        if sky is not None:
+            sb.set_sky(sky)
+        return sb
+
     @property
     def sky(self):
         return self._sky

@@ -18,9 +18,9 @@ for spec in "$@"; do
     git archive "$ref" paper_2507_16165_b200/csrc | tar -x -C "$src" --strip-components=2
   fi
   objs=""
-  for f in trace_reference trace_scene table shade bhrt_cuda fp64_peak; do
-    nvcc $ARCH $FL -I$src $defs -c $src/$f.cu -o build/variants/${name}_$f.o &
-    objs="$objs build/variants/${name}_$f.o"
+  for f in trace_reference.cu trace_scene.cu table.cu shade.cu bhrt_cuda.cu fp64_peak.cu scene_text.cpp; do
+    nvcc $ARCH $FL -I$src $defs -c $src/$f -o build/variants/${name}_${f%.*}.o &
+    objs="$objs build/variants/${name}_${f%.*}.o"
   done
   wait
   nvcc $ARCH -shared -o build/variants/lib_$name.so $objs -lcudart
