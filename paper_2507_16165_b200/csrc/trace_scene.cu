@@ -323,8 +323,13 @@ __device__ BHRT_INL_EVT bool step_events(const KParams& p, SceneSm& sm, int t, d
     const int nc = sm.nc[t];
     const bool test_all = nc < 0;
     unsigned act = 0;
+    unsigned ang = 0;  // candidates whose angular window meets the step
     if (!test_all) {
         const float fa = (float)pa, fb = (float)pb;
+        for (int i = 0; i < nc; ++i)
+            if (sm.lo[i][t] <= fb && sm.hi[i][t] >= fa) ang |= 1u << i;
+    }
+    if (ang) {
         // Conservative radial extent of the step's polyline. Its vertices lie
         // on the Hermite interpolant u(t), t in [0, 1], whose range is spanned
         // by the end values and the interior roots of u'(t) (fp32, widened by
@@ -364,9 +369,10 @@ __device__ BHRT_INL_EVT bool step_events(const KParams& p, SceneSm& sm, int t, d
             if (umax > 0.0f) slo = (1.0f / umax) * (1.0f - 0.5f * dl * dl) * (1.0f - 1e-5f);
             if (umin > 0.0f) shi = (1.0f / umin) * (1.0f + 1e-5f);
         }
-        for (int i = 0; i < nc; ++i)
-            if (sm.lo[i][t] <= fb && sm.hi[i][t] >= fa && sm.rlo[i][t] <= shi && sm.rhi[i][t] >= slo)
-                act |= 1u << i;
+        for (unsigned m = ang; m; m &= m - 1) {
+            const int i = __ffs(m) - 1;
+            if (sm.rlo[i][t] <= shi && sm.rhi[i][t] >= slo) act |= 1u << i;
+        }
     }
     bool sph_hit = false;
     int bsph = -1;
