@@ -243,6 +243,13 @@ int bhrt_ctx_set_scene(bhrt_ctx* ctx, const bhrt_scene* scene, bhrt_status_info*
 int bhrt_ctx_render_async(bhrt_ctx* ctx, int32_t row_start, int32_t row_end, int32_t tile_rows,
                           int32_t tile_stride, int32_t tile_offset, uint8_t* d_out,
                           bhrt_ray_record* d_records, void* stream, bhrt_status_info* info);
+/* Opens a frame of several render_async calls (e.g. row bands enqueued back
+ * to back so each band's copy-out overlaps the next band's kernel): counters
+ * and the lowest failing pixel are reset once here on `stream` and then
+ * accumulate over the frame's render_async calls (issue them on the same
+ * stream) until bhrt_ctx_finish, which reports the lowest failing pixel of
+ * the whole frame. Without it every render_async starts fresh. */
+int bhrt_ctx_frame_begin(bhrt_ctx* ctx, void* stream, bhrt_status_info* info);
 /* Waits for the context's last render on its stream and reports the lowest
  * failing pixel, if any. */
 int bhrt_ctx_finish(bhrt_ctx* ctx, bhrt_status_info* info);

@@ -207,7 +207,9 @@ struct bhrt_ctx {
     int launches = 0;
     int pending = 0;
     int32_t last_rows = 0;
-    unsigned long long host_stats[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    // pinned: [0..7] last render's counters (async D2H), [8..15] their reset pattern
+    unsigned long long* host_stats = nullptr;
+    bool in_frame = false;  // bhrt_ctx_frame_begin .. bhrt_ctx_finish: counters accumulate
     bool timing = false;
     bool timed = false;
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
@@ -352,6 +354,9 @@ int bhrt_ctx_create(int32_t device, bhrt_ctx** out, bhrt_status_info* info) {
     c->device = device;
     if (c->stats.ensure(8) || c->queue.ensure(1) || c->tables.ensure(2 * kQN))
         return set_info(info, BHRT_DEVICE, -1, -1, "bhrt_ctx_create: cudaMalloc failed");
+    CK(cudaMallocHost(&c->host_stats, 16 * sizeof(unsigned long long)));
+    for (int i = 0; i < 16; ++i) c->host_stats[i] = 0;
+    c->host_stats[3] = c->host_stats[11] = ULLONG_MAX;
     double tb[2 * kQN];
     factor_tables(tb, tb + kQN);
     CK(cudaMemcpy(c->tables.p, tb, sizeof tb, cudaMemcpyHostToDevice));
@@ -395,6 +400,7 @@ void bhrt_ctx_destroy(bhrt_ctx* c) {
     c->stats.release();
     c->queue.release();
     c->cull.release();
+    if (c->host_stats) cudaFreeHost(c->host_stats);
     c->tab_smp.release();
     c->tab_ends.release();
     c->tab_psi0.release();
@@ -554,15 +560,18 @@ int bhrt_ctx_render_async(bhrt_ctx* c, int32_t row_start, int32_t row_end, int32
     k.out = d_out;
     k.stats = c->stats.p;
     k.queue = c->queue.p;
-    const unsigned long long init[8] = {0ull, 0ull, 0ull, ULLONG_MAX, 0ull, 0ull, 0ull, 0ull};
-    CK(cudaMemcpyAsync(c->stats.p, init, sizeof init, cudaMemcpyHostToDevice, st));
+    if (!c->in_frame) {  // counters + lowest failing pixel start fresh for this render
+        CK(cudaMemcpyAsync(c->stats.p, c->host_stats + 8, 8 * sizeof(unsigned long long),
+                           cudaMemcpyHostToDevice, st));
+        c->launches = 0;
+    }
     CK(cudaMemsetAsync(c->queue.p, 0, sizeof(unsigned int), st));
-    c->launches = 0;
     c->timed = c->timing && rows > 0;
     if (rows > 0 && launch_trace(k, st, &c->launches, c->timed ? c->ev : nullptr) != 0)
         return set_info(info, BHRT_INVALID_ARGUMENT, -1, -1, "render: unsupported integrator");
     CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(c->host_stats, c->stats.p, sizeof c->host_stats, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(c->host_stats, c->stats.p, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                       st));
     c->last_stream = st;
     c->pending = 1;
     c->last_rows = rows;
@@ -575,18 +584,30 @@ int bhrt_ctx_render_async(bhrt_ctx* c, int32_t row_start, int32_t row_end, int32
     return 0;
 }
 
+int bhrt_ctx_frame_begin(bhrt_ctx* c, void* stream, bhrt_status_info* info) {
+    set_info(info, 0, -1, -1, "");
+    if (!c || !c->has_scene) return set_info(info, BHRT_INVALID_ARGUMENT, -1, -1, "context has no scene");
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    CK(cudaMemcpyAsync(c->stats.p, c->host_stats + 8, 8 * sizeof(unsigned long long), cudaMemcpyHostToDevice,
+                       st));
+    c->launches = 0;
+    c->in_frame = true;
+    return 0;
+}
+
 int bhrt_ctx_finish(bhrt_ctx* c, bhrt_status_info* info) {
     set_info(info, 0, -1, -1, "");
     if (!c) return set_info(info, BHRT_INVALID_ARGUMENT, -1, -1, "NULL context");
     CK(cudaSetDevice(c->device));
+    c->in_frame = false;
     if (!c->pending) return 0;
     CK(cudaStreamSynchronize(c->last_stream));
     c->pending = 0;
-    const unsigned long long fail = c->host_stats[3];
+    const unsigned long long fail = c->host_stats[3];  // lowest failing y * width + x
     if (fail != ULLONG_MAX) {
-        const int j = static_cast<int>(fail / c->kp.width);
+        const int py = static_cast<int>(fail / c->kp.width);
         const int px = static_cast<int>(fail % c->kp.width);
-        const int py = packed_row_to_y(c->kp, j);
         char msg[96];
         std::snprintf(msg, sizeof msg, "pixel (%d, %d): numerical failure", px, py);
         return set_info(info, BHRT_NUMERICAL, px, py, msg);

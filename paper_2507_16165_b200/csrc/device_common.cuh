@@ -347,7 +347,7 @@ __device__ __forceinline__ void finish_sample(const KParams& p, bool valid, cons
         const long long pix = id.rec / p.spp;
         uint8_t* o = p.out + 3 * pix;
         if (anybad) {
-            atomicMin(&p.stats[3], (unsigned long long)pix);
+            atomicMin(&p.stats[3], (unsigned long long)id.y * p.width + id.x);  // image order
             o[0] = o[1] = o[2] = 0;
         } else {
             store_pixel(o, acc, p.spp);

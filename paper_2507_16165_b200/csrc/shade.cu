@@ -27,8 +27,9 @@ __global__ void __launch_bounds__(256) shade_kernel(const __grid_constant__ KPar
     }
     uint8_t* o = p.out + 3 * i;
     if (failed) {
-        // lowest failing pixel in image order: packed rows are ordered by y
-        atomicMin(&p.stats[3], (unsigned long long)i);
+        // lowest failing pixel in image order (y * width + x)
+        const long long j = i / p.width;
+        atomicMin(&p.stats[3], (unsigned long long)packed_row_to_y(p, (int)j) * p.width + (i - j * p.width));
         o[0] = o[1] = o[2] = 0;
         return;
     }

@@ -58,6 +58,7 @@ def lib():
                                             C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
                                             C.c_void_p, P(StatusInfo)]
         L.bhrt_ctx_finish.argtypes = [C.c_void_p, P(StatusInfo)]
+        L.bhrt_ctx_frame_begin.argtypes = [C.c_void_p, C.c_void_p, P(StatusInfo)]
         L.bhrt_ctx_stats.argtypes = [C.c_void_p, P(C.c_uint64), P(C.c_uint64), P(C.c_uint64),
                                      P(C.c_int32)]
         L.bhrt_ctx_counters.argtypes = [C.c_void_p, P(C.c_uint64)]
@@ -78,7 +79,7 @@ EXPORTS = [
     "bhrt_scene_defaults", "bhrt_validate_scene", "bhrt_make_spheres", "bhrt_make_bands",
     "bhrt_cuda_render_rows", "bhrt_cuda_trace_rays", "bhrt_scene_parse_text",
     "bhrt_scene_format_text", "bhrt_ctx_create", "bhrt_ctx_destroy", "bhrt_ctx_set_scene",
-    "bhrt_ctx_render_async", "bhrt_ctx_finish", "bhrt_ctx_stats", "bhrt_ctx_set_timing",
+    "bhrt_ctx_render_async", "bhrt_ctx_frame_begin", "bhrt_ctx_finish", "bhrt_ctx_stats", "bhrt_ctx_set_timing",
     "bhrt_ctx_kernel_ms", "bhrt_ctx_counters", "bhrt_tile_row_count",
     "bhrt_b200_fp64_peak_tflops", "bhrt_cuda_abi_version", "bhrt_flops_per_step",
 ]

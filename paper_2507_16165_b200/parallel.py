@@ -106,12 +106,43 @@ class FrameRenderer:
     def finish(self):
         self.ctx.finish()
 
-    def render(self, scene):
-        """End-to-end: H2D scene, render, gather, D2H on rank 0."""
+    def render(self, scene, bands: int = 8):
+        """End-to-end: H2D scene, render, gather, D2H on rank 0. On one GPU
+        the frame is enqueued as `bands` row bands on the render stream and
+        each band's device->host copy runs on a copy stream as soon as its
+        kernel ends, so only the last band's copy is exposed."""
         self.set_scene(scene)
+        if self.world == 1 and bands > 1:
+            return self._render_banded(bands)
         img = self.render_device()
         if self.rank == 0:
             self.host.copy_(img, non_blocking=True)
         self.finish()
         torch.cuda.current_stream(self.device).synchronize()
         return self.host if self.rank == 0 else None
+
+    def _render_banded(self, bands: int):
+        h, w = self.scene.s.height, self.scene.s.width
+        st = torch.cuda.current_stream(self.device)
+        if getattr(self, "_copy_stream", None) is None:
+            self._copy_stream = torch.cuda.Stream(self.device)
+        cs = self._copy_stream
+        out = self.out.view(-1)
+        host = self.host.view(-1)
+        row_bytes = 3 * w
+        self.ctx.frame_begin(st.cuda_stream)
+        edges = [h * b // bands for b in range(bands + 1)]
+        for r0, r1 in zip(edges[:-1], edges[1:]):
+            if r1 == r0:
+                continue
+            self.ctx.render_async(out.data_ptr() + r0 * row_bytes, r0, r1, 1, 1, 0,
+                                  stream=st.cuda_stream)
+            ev = torch.cuda.Event()
+            ev.record(st)
+            cs.wait_event(ev)
+            with torch.cuda.stream(cs):
+                host[r0 * row_bytes:r1 * row_bytes].copy_(out[r0 * row_bytes:r1 * row_bytes],
+                                                          non_blocking=True)
+        cs.synchronize()
+        self.finish()
+        return self.host

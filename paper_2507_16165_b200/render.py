@@ -159,6 +159,12 @@ class Context:
                                                 C.c_void_p(stream or 0), C.byref(info))
         _raise(rc, info)
 
+    def frame_begin(self, stream: int | None = None):
+        """Counters/failures accumulate over the following render_async calls
+        (same stream) until finish() (bhrt_ctx_frame_begin)."""
+        info = StatusInfo()
+        _raise(native.lib().bhrt_ctx_frame_begin(self._h, C.c_void_p(stream or 0), C.byref(info)), info)
+
     def finish(self):
         info = StatusInfo()
         _raise(native.lib().bhrt_ctx_finish(self._h, C.byref(info)), info)

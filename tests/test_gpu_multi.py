@@ -81,3 +81,34 @@ def test_frame_renderer_two_ranks_share_one_gpu():
         p.join(300)
         assert p.exitcode == 0
     assert np.array_equal(img, full)
+
+
+def test_banded_end_to_end_render_matches_single_launch():
+    """FrameRenderer.render on one GPU enqueues row bands with overlapped
+    copy-out (bhrt_ctx_frame_begin): same bytes as one launch and as
+    render_rows."""
+    sb = scenes.config(2, 320, 180)
+    fr = parallel.FrameRenderer()
+    one = fr.render(sb, bands=1).clone()
+    for bands in (2, 7, 8, 180):
+        assert torch.equal(fr.render(sb, bands=bands), one)
+    assert np.array_equal(one.numpy().ravel(), render.render_rows(sb, 0, 180))
+
+
+def test_banded_render_reports_lowest_failing_pixel_of_the_frame():
+    """Camera looking away from the hole with wide windows (epsilon = 100):
+    near-radial outgoing rays leave u > 0 (geodesic.cpp:233-234). The
+    oracle's lowest failing pixel is (15, 7), in the second of eight bands;
+    the frame-level report must match however the frame is split."""
+    bg = scenes.gradient_background()
+    sb = scenes.small_scene(bg, 32, 1e-3)
+    cp = list(sb.s.cam_pos)
+    sb.set(cam_look_at=tuple(2 * c for c in cp), epsilon=100.0)
+    fr = parallel.FrameRenderer()
+    for bands in (1, 8, 32):
+        with pytest.raises(render.RenderError) as e:
+            fr.render(sb, bands=bands)
+        assert (e.value.px, e.value.py) == (15, 7)
+    with pytest.raises(render.RenderError) as e:
+        render.render_rows(sb, 0, 32)
+    assert (e.value.px, e.value.py) == (15, 7)
