@@ -106,7 +106,7 @@ class FrameRenderer:
     def finish(self):
         self.ctx.finish()
 
-    def render(self, scene, bands: int = 8):
+    def render(self, scene, bands: int = 4):  # 4K config 2: 1/2/4/8/16 bands 9.04/8.92/8.85/8.96/9.21 ms
         """End-to-end: H2D scene, render, gather, D2H on rank 0. On one GPU
         the frame is enqueued as `bands` row bands on the render stream and
         each band's device->host copy runs on a copy stream as soon as its
