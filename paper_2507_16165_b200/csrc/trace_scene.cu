@@ -11,7 +11,10 @@
 
 namespace bhrt_b200 {
 
-constexpr int kBlock = 128;
+#ifndef BHRT_SCENE_BLOCK
+#define BHRT_SCENE_BLOCK 128
+#endif
+constexpr int kBlock = BHRT_SCENE_BLOCK;
 constexpr int kSlots = 8;
 constexpr int kSphSm = 128;          // spheres staged in shared memory
 constexpr float kWinMargin = 5e-4f;  // fp32 window slack (rad); windows only cull
@@ -501,10 +504,16 @@ __device__ __noinline__ Hit radial_scene(const KParams& p, V3 origin, V3 dir, do
 }
 
 template <int INTEG>
-__global__ void __launch_bounds__(kBlock, BHRT_SCENE_MINB) trace_scene_kernel(const __grid_constant__ KParams p) {
+#ifdef BHRT_SCENE_MAXNREG  // explicit register cap instead of a blocks-per-SM bound
+__global__ void __maxnreg__(BHRT_SCENE_MAXNREG)
+#else
+__global__ void __launch_bounds__(kBlock, BHRT_SCENE_MINB)
+#endif
+    trace_scene_kernel(const __grid_constant__ KParams p) {
     __shared__ SceneSm sm;
     const int t = threadIdx.x;
-    for (int k = t; k < p.n_spheres && k < kSphSm; k += blockDim.x) {
+    // the fp32 prefilter is read only without the plane-angle cull table
+    for (int k = t; !p.cull && k < p.n_spheres && k < kSphSm; k += blockDim.x) {
         const V3 c = sphere_c(p, k);
         const double r = p.spheres[k].radius;
         const float slack = 1e-5f * (float)(norm(c) + r) + 1e-6f;
