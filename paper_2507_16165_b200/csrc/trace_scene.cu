@@ -306,23 +306,17 @@ __device__ BHRT_INL_EVT bool step_events(const KParams& p, SceneSm& sm, int t, d
 #ifdef BHRT_COUNTERS
     atomicAdd(&p.stats[7], 1ull);
 #endif
-    // ---- disk
+    // ---- disk (only the radius is kept across the sphere search; the disk
+    // line is formed after it, so little stays live across that call)
     bool disk_hit = false;
-    double r_ev = 0.0, dlx = 0.0, dly = 0.0;
-    V3 Lw = mk(0.0, 0.0, 0.0);
+    double r_ev;
     const double sigma = sm.sigma[t];
     if (next_disk > pa && next_disk <= pb) {
         const double tt = (next_disk - pa) / h;
         const double u_ev = hermite_eval(cu, tt);
         if (u_ev > 0.0) {
             r_ev = 1.0 / u_ev;
-            if (r_ev >= p.disk_r_in && r_ev <= p.disk_r_out) {
-                disk_hit = true;
-                double ux, uy;
-                disk_line(sm, t, ux, uy, Lw);
-                dlx = sigma * ux;
-                dly = sigma * uy;
-            }
+            disk_hit = r_ev >= p.disk_r_in && r_ev <= p.disk_r_out;
         }
     }
     // ---- spheres
@@ -381,8 +375,8 @@ __device__ BHRT_INL_EVT bool step_events(const KParams& p, SceneSm& sm, int t, d
         }
     }
     bool sph_hit = false;
-    int bsph = -1;
-    double bqx = 0.0, bqy = 0.0;
+    int bsph;          // outputs of sphere_search, read only when sph_hit
+    double bqx, bqy;
     if (act || test_all) {
         sph_hit = sphere_search(p, sm, t, pa, h, ua, ub, cu, act, nc, bsph, bqx, bqy);
         if (sph_hit) {
@@ -394,16 +388,22 @@ __device__ BHRT_INL_EVT bool step_events(const KParams& p, SceneSm& sm, int t, d
         atomicAdd(&p.stats[5], (unsigned long long)__popc(act));
 #endif
     }
-    if (sph_hit && disk_hit) {
-        if (bqx * dly - bqy * dlx > 0.0)
-            disk_hit = false;
-        else
-            sph_hit = false;
+    if (disk_hit) {
+        double ux, uy;
+        V3 Lw;
+        disk_line(sm, t, ux, uy, Lw);
+        if (sph_hit) {
+            const double dlx = sigma * ux, dly = sigma * uy;
+            if (bqx * dly - bqy * dlx > 0.0)
+                disk_hit = false;
+            else
+                sph_hit = false;
+        }
+        if (disk_hit) hit.point = add(vld(p.center), scl(Lw, sigma * r_ev));
     }
     if (disk_hit) {
         hit.obj = BHRT_OBJ_DISK;
         hit.sphere = -1;
-        hit.point = add(vld(p.center), scl(Lw, sigma * r_ev));
     } else if (sph_hit) {
         hit.obj = BHRT_OBJ_SPHERE;
         hit.sphere = bsph;
