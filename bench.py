@@ -190,6 +190,28 @@ def measure_secondary(device: int, reps: int = 3) -> dict:
                       "Mrays/s": frames * sb0.s.width * sb0.s.height * sb0.s.spp / dt / 1e6,
                       "size": [sb0.s.width, sb0.s.height, sb0.s.spp],
                       "note": "1 GPU; frames shard f mod N across GPUs"}
+    # the reference's own algorithm (mode R: DOPRI5 in eps-windows, its
+    # arithmetic) on the GPU, on the same sky-only projection of config 2 that
+    # `reference_sky_only` times on the CPU: same algorithm, same bytes
+    proj = scenes.sky_only_projection(scenes.config(2))
+    ctx.set_scene(proj)
+    buf = torch.empty(proj.s.width * proj.s.height * 3, dtype=torch.uint8, device="cuda")
+    ctx.render_async(buf.data_ptr(), 1000, 1016, stream=st.cuda_stream)  # warm-up band
+    ctx.finish()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    ctx.render_async(buf.data_ptr(), stream=st.cuda_stream)
+    e1.record(st)
+    ctx.finish()
+    ms = e0.elapsed_time(e1)
+    rays = proj.s.width * proj.s.height * proj.s.spp
+    out["modeR_sky_only"] = {"ms": ms, "Mrays/s": rays / ms / 1e3,
+                             "windows_per_ray": ctx.stats()["steps"] / rays,
+                             "size": [proj.s.width, proj.s.height, proj.s.spp],
+                             "note": "trace_reference_kernel (reference algorithm, bit-identical "
+                                     "window arithmetic) on the full sky-only projection; compare "
+                                     "reference_sky_only (the reference on the host cores)"}
     ctx.close()
     return out
 
