@@ -450,6 +450,7 @@ int bhrt_ctx_set_scene(bhrt_ctx* c, const bhrt_scene* s, bhrt_status_info* info)
     k.epsilon = s->epsilon;
     k.rel_tol = s->rel_tol;
     k.abs_tol = s->abs_tol;
+    k.ref_pow_prev0 = std::pow(1e-4, 0.4 / 5.0);  // host libm, as the reference
     k.step = s->step;
     k.max_step = s->max_step;
     k.chord_dphi = s->chord_dphi;
@@ -792,6 +793,7 @@ extern "C" int bhrt_cuda_trace_rays(const bhrt_scene* s, const double* rays, int
     k.epsilon = s->epsilon;
     k.rel_tol = s->rel_tol;
     k.abs_tol = s->abs_tol;
+    k.ref_pow_prev0 = std::pow(1e-4, 0.4 / 5.0);  // host libm, as the reference
     CK(cudaMemcpy(c->rays.p, rays, sizeof(double) * 6 * n, cudaMemcpyHostToDevice));
     launch_trace_rays(k, c->rays.p, n, c->records.p, deflection ? c->defl.p : nullptr, nullptr);
     CK(cudaGetLastError());

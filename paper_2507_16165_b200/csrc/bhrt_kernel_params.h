@@ -36,6 +36,10 @@ struct KParams {
     uint64_t seed;
     // integrator
     double epsilon, rel_tol, abs_tol, step, max_step, chord_dphi;
+    // mode R: pow(1e-4, 0.4 / 5) with the HOST libm, i.e. the value the
+    // reference's PI factor uses on the first step of every window, where
+    // err_prev = 1e-4 (geodesic.cpp:107,144-151)
+    double ref_pow_prev0;
     // rows: packed row j -> image row y (see bhrt_ctx_render_async)
     int32_t row_start, row_end, tile_rows, tile_stride, tile_offset, n_rows;
     // sky
