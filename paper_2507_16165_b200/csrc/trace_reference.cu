@@ -43,17 +43,44 @@ __device__ __forceinline__ double rhs_w(double u, double mass) { return 3.0 * ma
 
 // geodesic.cpp:84-162. Returns false on StepSizeUnderflow (phi/u/w then hold
 // the failure state, as StepSizeUnderflow::state does).
-// pow_prev0 = pow(1e-4, 0.4 / 5) from the host libm: the err_prev factor of
-// the first step of each window (err_prev starts at 1e-4), which is ~99% of
-// all steps (1.007 steps per window) — one device pow per step saved, the
-// same double the reference multiplies by.
+// The step hint carried from one window to the next (geodesic.cpp:106,160):
+// hint = h_try * clamp(0.9 * err^-0.14 * err_prev^0.08, 0.2, 5) of the
+// window's last (accepted) step. It only matters when it is below the next
+// window's dphi; it is kept as its inputs and evaluated lazily (below).
+struct HintState {
+    double h_try, err, pprev;  // last accepted step, its error norm, err_prev^0.08
+    bool pending;              // false: no hint yet (hint = 0 in the reference)
+};
+
+// First step size of a window: min(hint, dphi), or dphi without a hint.
+// A fp32 lower bound of the PI factor (|error| << the 0.1% margin) decides
+// whether hint >= dphi for sure — then min(hint, dphi) = dphi exactly and
+// the device pow is skipped; otherwise the exact double is formed.
+__device__ __forceinline__ double window_h0(const HintState& hs, double dphi) {
+    if (!hs.pending) return dphi;
+    const float ef = (float)hs.err;
+    if (ef > 1e-30f && ef <= 1.0f) {
+        const float lf = 0.9f * exp2f(-0.14f * __log2f(ef)) * (float)hs.pprev;
+        const float lo = fminf(fmaxf(lf * 0.999f, 0.2f), 5.0f);
+        if ((float)hs.h_try * lo >= (float)dphi * 1.00001f) return dphi;
+    }
+    const double factor = clampd(0.9 * pow(hs.err, -0.7 / 5.0) * hs.pprev, 0.2, 5.0);
+    const double hint = hs.h_try * factor;
+    return hint > 0.0 ? dmin(hint, dphi) : dphi;
+}
+
+// geodesic.cpp:84-162. Returns false on StepSizeUnderflow (phi/u/w then hold
+// the failure state, as StepSizeUnderflow::state does). pow_prev0 =
+// pow(1e-4, 0.4 / 5) from the host libm: the err_prev factor of the first
+// step of each window (err_prev starts at 1e-4) — the same double the
+// reference multiplies by, without a device pow.
 __device__ bool integrate_window(double& phi, double& u, double& w, double dphi, double mass,
-                                 double rtol, double atol, double& hint, unsigned& nsteps,
+                                 double rtol, double atol, HintState& hs, unsigned& nsteps,
                                  unsigned& nrej, double pow_prev0) {
     double y0 = u, y1 = w;
     double k10 = y1, k11 = rhs_w(y0, mass);
     double remaining = dphi;
-    double h = hint > 0.0 ? dmin(hint, dphi) : dphi;
+    double h = window_h0(hs, dphi);
     double err_prev = 1e-4;
     double pprev = pow_prev0;  // pow(err_prev, 0.4 / 5)
     while (remaining > 0.0) {
@@ -91,11 +118,14 @@ __device__ bool integrate_window(double& phi, double& u, double& w, double dphi,
             k10 = k70;
             k11 = k71;
             remaining -= h_try;
-            const double factor = clampd(0.9 * pow(err, -0.7 / 5.0) * pprev, 0.2, 5.0);
-            h = h_try * factor;
-            err_prev = dmax(err, 1e-4);
-            if (remaining > 0.0) pprev = pow(err_prev, 0.4 / 5.0);  // needed only within this window
             ++nsteps;
+            if (!(remaining > 0.0)) {  // window done: the hint is formed lazily (window_h0)
+                hs = {h_try, err, pprev, true};
+                break;
+            }
+            h = h_try * clampd(0.9 * pow(err, -0.7 / 5.0) * pprev, 0.2, 5.0);
+            err_prev = dmax(err, 1e-4);
+            pprev = pow(err_prev, 0.4 / 5.0);
         } else {
             h = h_try * clampd(0.9 * pow(err, -0.2), 0.1, 0.9);
             ++nrej;
@@ -107,7 +137,6 @@ __device__ bool integrate_window(double& phi, double& u, double& w, double dphi,
             return false;
         }
     }
-    hint = h;
     phi = phi + dphi;
     u = y0;
     w = y1;
@@ -140,7 +169,8 @@ __device__ __forceinline__ RResult window_loop(const KParams& p, V3 origin, V3 c
     R.edir = mk(0.0, 0.0, 0.0);
     R.chord = false;
     R.defl = 0.0;
-    double phi = 0.0, hint = 0.0;
+    double phi = 0.0;
+    HintState hs{0.0, 0.0, 0.0, false};
     double prev_phi = 0.0, prev_u = 0.0, last_phi = 0.0, last_u = 0.0;
     int npts = 1;
     V3 p_prev = origin;
@@ -161,7 +191,7 @@ __device__ __forceinline__ RResult window_loop(const KParams& p, V3 origin, V3 c
         // segment_dphi, geodesic.cpp:76-80
         const double hyp = glibc_hypot(u, w);
         const double dphi = clampd(p.epsilon * u * u / hyp, 1e-6, 0.1);
-        if (!integrate_window(phi, u, w, dphi, p.mass, p.rel_tol, p.abs_tol, hint, nsteps, nrej,
+        if (!integrate_window(phi, u, w, dphi, p.mass, p.rel_tol, p.abs_tol, hs, nsteps, nrej,
                               p.ref_pow_prev0)) {
             if (p.mass > 0.0 && u >= p.u_cap) { R.obj = BHRT_OBJ_HORIZON; break; }
             R.obj = -BHRT_NUMERICAL;

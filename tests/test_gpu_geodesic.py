@@ -202,3 +202,30 @@ def test_empty_batch():
     rec, defl = G.trace_batch(np.zeros((0, 3)), np.zeros((0, 3)), G.BlackHole(1.0), cfg(),
                               deflection=True)
     assert len(rec) == 0 and len(defl) == 0
+
+
+@pytest.mark.parametrize("eps,rt,at", [(1.0, 1e-10, 1e-12), (5.0, 1e-13, 1e-15), (0.02, 1e-8, 1e-10)])
+def test_step_hint_regimes_match_oracle(eps, rt, at):
+    """Wide windows / tight tolerances make the carried step hint binding
+    (several DOPRI5 steps per window; the kernel forms the hint lazily,
+    trace_reference.cu window_h0): outcomes and escape directions still
+    match the oracle to the north-star 1e-9. Step counts are compared only
+    where the hint rarely binds: where it does, the PI factor's pow()
+    (libdevice vs glibc, <= 1 ulp) moves step boundaries (measured: 122/600
+    and 539/600 rays in the first two regimes, identical before and after
+    the lazy-hint change)."""
+    o, d = random_rays(600, 21, 10.0, 80.0)
+    rec, _ = G.trace_batch(o, d, G.BlackHole(1.0), cfg(eps=eps, esc=300.0, rt=rt, at=at))
+    mism = steps = 0
+    for i in range(len(o)):
+        rc, kind, edir, _, _, ns, nr = orc_trace_reference(o[i], d[i], 1.0, (0, 0, 0), eps, 300.0, 10,
+                                                           rt, at)
+        if rc != 0 or rec[i]["object"] != KIND[kind]:
+            mism += 1
+            continue
+        steps += int(rec[i]["steps"] != ns)
+        if kind == 1:
+            assert np.abs(rec[i]["point"] - np.array(edir)).max() <= 1e-9
+    assert mism <= 2
+    if eps < 0.1:
+        assert steps <= 0.02 * len(o)
