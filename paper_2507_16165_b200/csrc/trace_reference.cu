@@ -47,6 +47,9 @@ __device__ __forceinline__ double rhs_w(double u, double mass) { return 3.0 * ma
 // hint = h_try * clamp(0.9 * err^-0.14 * err_prev^0.08, 0.2, 5) of the
 // window's last (accepted) step. It only matters when it is below the next
 // window's dphi; it is kept as its inputs and evaluated lazily (below).
+#ifdef BHRT_HINT_COUNT
+__device__ unsigned long long g_hint_count[4];  // developer counters: exact hints, binding hints, multi-step windows
+#endif
 struct HintState {
     double h_try, err, pprev;  // last accepted step, its error norm, err_prev^0.08
     bool pending;              // false: no hint yet (hint = 0 in the reference)
@@ -59,13 +62,22 @@ struct HintState {
 __device__ __forceinline__ double window_h0(const HintState& hs, double dphi) {
     if (!hs.pending) return dphi;
     const float ef = (float)hs.err;
-    if (ef > 1e-30f && ef <= 1.0f) {
-        const float lf = 0.9f * exp2f(-0.14f * __log2f(ef)) * (float)hs.pprev;
-        const float lo = fminf(fmaxf(lf * 0.999f, 0.2f), 5.0f);
+    if (hs.err >= 0.0 && ef <= 1.0f) {
+        // err <= 1e-30: err^-0.14 >= 1.58e4, pprev >= 1e-4^0.08 = 0.48, so the
+        // factor is clamped to exactly 5 (also for err = 0: pow -> inf)
+        float lo = 5.0f;
+        if (ef > 1e-30f) {
+            const float lf = 0.9f * exp2f(-0.14f * __log2f(ef)) * (float)hs.pprev;
+            lo = fminf(fmaxf(lf * 0.999f, 0.2f), 5.0f);
+        }
         if ((float)hs.h_try * lo >= (float)dphi * 1.00001f) return dphi;
     }
     const double factor = clampd(0.9 * pow(hs.err, -0.7 / 5.0) * hs.pprev, 0.2, 5.0);
     const double hint = hs.h_try * factor;
+#ifdef BHRT_HINT_COUNT
+    atomicAdd(&g_hint_count[0], 1ull);
+    if (hint < dphi) atomicAdd(&g_hint_count[1], 1ull);
+#endif
     return hint > 0.0 ? dmin(hint, dphi) : dphi;
 }
 
@@ -123,6 +135,9 @@ __device__ bool integrate_window(double& phi, double& u, double& w, double dphi,
                 hs = {h_try, err, pprev, true};
                 break;
             }
+#ifdef BHRT_HINT_COUNT
+            atomicAdd(&g_hint_count[2], 1ull);
+#endif
             h = h_try * clampd(0.9 * pow(err, -0.7 / 5.0) * pprev, 0.2, 5.0);
             err_prev = dmax(err, 1e-4);
             pprev = pow(err_prev, 0.4 / 5.0);
@@ -299,6 +314,12 @@ void launch_trace_rays(const KParams& p, const double* rays, long long n, bhrt_r
     else
         trace_rays_kernel<false><<<blocks, 128, 0, st>>>(p, rays, n, records, nullptr);
 }
+
+#ifdef BHRT_HINT_COUNT
+extern "C" void bhrt_debug_hint_counts(unsigned long long out[4]) {
+    cudaMemcpyFromSymbol(out, g_hint_count, sizeof(unsigned long long) * 4);
+}
+#endif
 
 void launch_reference(const KParams& p, cudaStream_t st) {
     const long long n = (long long)p.n_rows * p.width * p.spp;
