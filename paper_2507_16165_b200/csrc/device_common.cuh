@@ -86,7 +86,8 @@ __device__ __forceinline__ double hypot_kernel(double ax, double ay) {
         t1 = 2.0 * delta * (ax - 2.0 * ay);
         t2 = (4.0 * delta - ay) * ay + delta * delta;
     }
-    h -= (t1 + t2) / (2.0 * h);
+    const double c = t1 + t2;
+    if (c != 0.0) h -= c / (2.0 * h);  // c = +-0: h - (+-0) = h; skips the division's zero slow path
     return h;
 }
 __device__ inline double glibc_hypot(double x, double y) {

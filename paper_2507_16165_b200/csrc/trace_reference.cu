@@ -121,9 +121,19 @@ __device__ bool integrate_window(double& phi, double& u, double& w, double dphi,
         const double s0 = atol + rtol * dmax(fabs(y0), fabs(n0));
         const double s1 = atol + rtol * dmax(fabs(y1), fabs(n1));
         double err = 0.0;
-        err += (e0 / s0) * (e0 / s0);
-        err += (e1 / s1) * (e1 / s1);
-        err = sqrt(err / 2.0);
+        const double tiny = 1e-42 * atol;
+        if (fabs(e0) < tiny && fabs(e1) < tiny) {
+            // s >= atol, so the norm is < 1e-42 < 1e-30. Every later use of
+            // err is then independent of its value: the step is accepted, the
+            // PI factor clamps to exactly 5 (err^-0.14 > 1.5e4, err_prev^0.08
+            // >= 0.48), err_prev becomes 1e-4. 0 stands in for it, sparing
+            // the divisions' and sqrt's denormal slow paths (frequent for
+            // near-linear far-field windows). NaNs fail the test above.
+        } else {
+            err += (e0 / s0) * (e0 / s0);
+            err += (e1 / s1) * (e1 / s1);
+            err = sqrt(err / 2.0);
+        }
         if (err <= 1.0) {
             y0 = n0;
             y1 = n1;
