@@ -190,6 +190,20 @@ def measure_secondary(device: int, reps: int = 3) -> dict:
                       "Mrays/s": frames * sb0.s.width * sb0.s.height * sb0.s.spp / dt / 1e6,
                       "size": [sb0.s.width, sb0.s.height, sb0.s.spp],
                       "note": "1 GPU; frames shard f mod N across GPUs"}
+    # the same orbit written out as PPM files (the host output pipeline,
+    # sequence.SequenceRenderer: kernel of frame f overlaps writing f-1)
+    import tempfile
+
+    from paper_2507_16165_b200.sequence import SequenceRenderer
+    with tempfile.TemporaryDirectory() as tmp:
+        paths = [os.path.join(tmp, f"frame_{f:04d}.ppm") for f in range(frames)]
+        sr = SequenceRenderer(device)
+        sr.render(scs[:2], paths[:2])  # warm-up
+        res = sr.render(scs, paths)
+        sr.close()
+    out["config4_ppm"] = {"frames": frames, "seconds": res["seconds"], "frames/s": res["frames/s"],
+                          "note": "render + D2H + PPM encode/write of every frame (save_ppm "
+                                  "layout), writer thread overlapped with the next frame's kernel"}
     # the reference's own algorithm (mode R: DOPRI5 in eps-windows, its
     # arithmetic) on the GPU, on the same sky-only projection of config 2 that
     # `reference_sky_only` times on the CPU: same algorithm, same bytes

@@ -230,6 +230,15 @@ double ref_strong_scaling_mean(const bhrt_scene* s, int threads, int repeats) {
     return mean;
 }
 
+// image.cpp:107-113 save_ppm of a w x h RGB8 image. Returns the size;
+// writes when cap is large enough.
+size_t ref_save_ppm(int w, int h, const std::uint8_t* rgb, std::uint8_t* out, size_t cap) {
+    std::vector<std::uint8_t> px(rgb, rgb + 3 * static_cast<size_t>(w) * h);
+    const std::vector<std::uint8_t> b = save_ppm(ImageBuffer(w, h, std::move(px)));
+    if (out && cap >= b.size()) std::memcpy(out, b.data(), b.size());
+    return b.size();
+}
+
 // config.cpp:96-112 serialize_scene of the scene's reference fields.
 // Returns the text length; writes when cap is large enough.
 size_t ref_serialize_scene(const bhrt_scene* s, char* buf, size_t cap) {

@@ -97,6 +97,8 @@ def ref():
         L.ref_serialize_scene.restype = C.c_size_t
         L.ref_serialize_scene.argtypes = [P(Scene), C.c_char_p, C.c_size_t]
         L.ref_parse_scene.argtypes = [C.c_char_p, P(Scene), P(StatusInfo)]
+        L.ref_save_ppm.restype = C.c_size_t
+        L.ref_save_ppm.argtypes = [C.c_int, C.c_int, P(C.c_uint8), P(C.c_uint8), C.c_size_t]
         _ref = L
     return _ref
 
