@@ -266,6 +266,23 @@ int bhrt_ctx_counters(bhrt_ctx* ctx, uint64_t out[8]);
  * last render's trace and shade kernels on the render stream. */
 int bhrt_ctx_set_timing(bhrt_ctx* ctx, int32_t enable);
 int bhrt_ctx_kernel_ms(bhrt_ctx* ctx, float* trace_ms, float* shade_ms);
+/* Output layout of subsequent renders: 0 (default) = rows packed in order
+ * of y into d_out; 1 = d_out is the whole image (height x width x 3) and each
+ * rendered row lands at its image position — with d_out a peer GPU's image
+ * buffer opened by bhrt_ipc_open, the ranks of a frame write their rows
+ * straight into rank 0's image over NVLink and no gather follows. */
+int bhrt_ctx_set_output_layout(bhrt_ctx* ctx, int32_t image_layout);
+
+/* Device buffers shareable across processes (CUDA IPC over NVLink/NVSwitch
+ * peer memory). bhrt_device_alloc: cudaMalloc on `device`; bhrt_ipc_export:
+ * 64-byte handle of such a buffer; bhrt_ipc_open: map a peer process's buffer
+ * on `device` (peer access enabled lazily); bhrt_ipc_close unmaps it. */
+int bhrt_device_alloc(int32_t device, size_t bytes, void** d_ptr, bhrt_status_info* info);
+int bhrt_device_free(int32_t device, void* d_ptr);
+int bhrt_ipc_export(int32_t device, void* d_ptr, uint8_t handle[64], bhrt_status_info* info);
+int bhrt_ipc_open(int32_t device, const uint8_t handle[64], void** d_ptr, bhrt_status_info* info);
+int bhrt_ipc_close(int32_t device, void* d_ptr);
+
 /* Number of rows selected by the tiling rule above. */
 int32_t bhrt_tile_row_count(int32_t row_start, int32_t row_end, int32_t tile_rows,
                             int32_t tile_stride, int32_t tile_offset);

@@ -210,6 +210,7 @@ struct bhrt_ctx {
     // pinned: [0..7] last render's counters (async D2H), [8..15] their reset pattern
     unsigned long long* host_stats = nullptr;
     bool in_frame = false;  // bhrt_ctx_frame_begin .. bhrt_ctx_finish: counters accumulate
+    int32_t out_image = 0;  // bhrt_ctx_set_output_layout
     bool timing = false;
     bool timed = false;
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
@@ -559,6 +560,7 @@ int bhrt_ctx_render_async(bhrt_ctx* c, int32_t row_start, int32_t row_end, int32
     }
     k.records = d_records;
     k.out = d_out;
+    k.out_image = c->out_image;
     k.stats = c->stats.p;
     k.queue = c->queue.p;
     if (!c->in_frame) {  // counters + lowest failing pixel start fresh for this render
@@ -582,6 +584,53 @@ int bhrt_ctx_render_async(bhrt_ctx* c, int32_t row_start, int32_t row_end, int32
     c->kp.tile_stride = tile_stride;
     c->kp.tile_offset = tile_offset;
     c->kp.n_rows = rows;
+    return 0;
+}
+
+int bhrt_ctx_set_output_layout(bhrt_ctx* c, int32_t image_layout) {
+    if (!c || image_layout < 0 || image_layout > 1) return BHRT_INVALID_ARGUMENT;
+    c->out_image = image_layout;
+    return 0;
+}
+
+int bhrt_device_alloc(int32_t device, size_t bytes, void** d_ptr, bhrt_status_info* info) {
+    set_info(info, 0, -1, -1, "");
+    if (!d_ptr) return set_info(info, BHRT_INVALID_ARGUMENT, -1, -1, "NULL output pointer");
+    CK(cudaSetDevice(device));
+    CK(cudaMalloc(d_ptr, bytes ? bytes : 1));
+    return 0;
+}
+
+int bhrt_device_free(int32_t device, void* d_ptr) {
+    bhrt_status_info* info = nullptr;
+    CK(cudaSetDevice(device));
+    CK(cudaFree(d_ptr));
+    return 0;
+}
+
+int bhrt_ipc_export(int32_t device, void* d_ptr, uint8_t handle[64], bhrt_status_info* info) {
+    set_info(info, 0, -1, -1, "");
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "CUDA IPC handle size");
+    CK(cudaSetDevice(device));
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, d_ptr));
+    std::memcpy(handle, &h, sizeof h);
+    return 0;
+}
+
+int bhrt_ipc_open(int32_t device, const uint8_t handle[64], void** d_ptr, bhrt_status_info* info) {
+    set_info(info, 0, -1, -1, "");
+    CK(cudaSetDevice(device));
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof h);
+    CK(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return 0;
+}
+
+int bhrt_ipc_close(int32_t device, void* d_ptr) {
+    bhrt_status_info* info = nullptr;
+    CK(cudaSetDevice(device));
+    CK(cudaIpcCloseMemHandle(d_ptr));
     return 0;
 }
 

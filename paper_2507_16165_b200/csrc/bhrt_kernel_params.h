@@ -73,7 +73,11 @@ struct KParams {
     // 1: shade inside the trace kernel (spp divides 32; the spp samples of a
     // pixel are adjacent lanes, summed in sample order by warp shuffles)
     int32_t fused_shade;
-    int32_t pad2;
+    // 0: `out` holds the rendered rows packed in order of y; 1: `out` is the
+    // whole image and pixel (x, y) lands at 3 (y width + x) — e.g. a peer
+    // GPU's image buffer mapped over NVLink (bhrt_ipc_open), so a rank's rows
+    // need no gather
+    int32_t out_image;
     // b-table (approximate mode): per entry kind/n, ends
     // {psi_end, u_end, w_end, psi_esc}, (u, u') samples at psi_j = j*dpsi with
     // a fixed stride of table_ns samples, and the frame's inbound psi of u0.

@@ -346,7 +346,7 @@ __device__ __forceinline__ void finish_sample(const KParams& p, bool valid, cons
     }
     if (valid && id.s == 0) {
         const long long pix = id.rec / p.spp;
-        uint8_t* o = p.out + 3 * pix;
+        uint8_t* o = p.out + 3 * (p.out_image ? (long long)id.y * p.width + id.x : pix);
         if (anybad) {
             atomicMin(&p.stats[3], (unsigned long long)id.y * p.width + id.x);  // image order
             o[0] = o[1] = o[2] = 0;

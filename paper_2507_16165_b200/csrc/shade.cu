@@ -25,7 +25,10 @@ __global__ void __launch_bounds__(256) shade_kernel(const __grid_constant__ KPar
         acc[1] += c[1];
         acc[2] += c[2];
     }
-    uint8_t* o = p.out + 3 * i;
+    const long long jrow = i / p.width;
+    uint8_t* o = p.out + 3 * (p.out_image ? (long long)packed_row_to_y(p, (int)jrow) * p.width +
+                                                (i - jrow * p.width)
+                                          : i);
     if (failed) {
         // lowest failing pixel in image order (y * width + x)
         const long long j = i / p.width;

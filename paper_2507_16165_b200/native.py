@@ -50,6 +50,12 @@ def lib():
         L.bhrt_scene_parse_text.argtypes = [C.c_char_p, P(Scene), P(Sphere), C.c_int32,
                                             P(C.c_int32), P(StatusInfo)]
         L.bhrt_scene_format_text.argtypes = [P(Scene), C.c_char_p, C.c_size_t, P(C.c_size_t)]
+        L.bhrt_ctx_set_output_layout.argtypes = [C.c_void_p, C.c_int32]
+        L.bhrt_device_alloc.argtypes = [C.c_int32, C.c_size_t, P(C.c_void_p), P(StatusInfo)]
+        L.bhrt_device_free.argtypes = [C.c_int32, C.c_void_p]
+        L.bhrt_ipc_export.argtypes = [C.c_int32, C.c_void_p, P(C.c_uint8), P(StatusInfo)]
+        L.bhrt_ipc_open.argtypes = [C.c_int32, P(C.c_uint8), P(C.c_void_p), P(StatusInfo)]
+        L.bhrt_ipc_close.argtypes = [C.c_int32, C.c_void_p]
         L.bhrt_ctx_create.argtypes = [C.c_int32, P(C.c_void_p), P(StatusInfo)]
         L.bhrt_ctx_destroy.argtypes = [C.c_void_p]
         L.bhrt_ctx_destroy.restype = None
@@ -78,7 +84,8 @@ def lib():
 EXPORTS = [
     "bhrt_scene_defaults", "bhrt_validate_scene", "bhrt_make_spheres", "bhrt_make_bands",
     "bhrt_cuda_render_rows", "bhrt_cuda_trace_rays", "bhrt_scene_parse_text",
-    "bhrt_scene_format_text", "bhrt_ctx_create", "bhrt_ctx_destroy", "bhrt_ctx_set_scene",
+    "bhrt_scene_format_text", "bhrt_ctx_set_output_layout", "bhrt_device_alloc",
+    "bhrt_device_free", "bhrt_ipc_export", "bhrt_ipc_open", "bhrt_ipc_close", "bhrt_ctx_create", "bhrt_ctx_destroy", "bhrt_ctx_set_scene",
     "bhrt_ctx_render_async", "bhrt_ctx_frame_begin", "bhrt_ctx_finish", "bhrt_ctx_stats", "bhrt_ctx_set_timing",
     "bhrt_ctx_kernel_ms", "bhrt_ctx_counters", "bhrt_tile_row_count",
     "bhrt_b200_fp64_peak_tflops", "bhrt_cuda_abi_version", "bhrt_flops_per_step",

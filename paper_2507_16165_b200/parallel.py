@@ -1,5 +1,7 @@
-"""Multi-GPU frame rendering: one process per GPU, cyclic row tiles, NCCL
-gather of the finished RGB8 rows to rank 0.
+"""Multi-GPU frame rendering: one process per GPU, cyclic row tiles; the
+finished RGB8 rows reach rank 0 either written straight into rank 0's image
+by each rank's kernel over NVLink peer memory (CUDA IPC, `peer=True`: no
+gather pass at all), or by an NCCL gather + unshuffle.
 
 The reference shards a frame into contiguous scanline bands over TCP
 workers (render.cpp:51-66, netrender.cpp:26-105). Rays are independent, so
@@ -9,10 +11,56 @@ cyclic rows reach 7.8x (SURVEY §2.3), hence row y -> rank (y // T) % N.
 """
 from __future__ import annotations
 
+import ctypes as C
+
 import torch
 import torch.distributed as dist
 
+from . import native
+from .abi import StatusInfo
 from .render import Context, tile_row_count
+
+
+class _DevArray:
+    """Zero-copy torch view of a raw device buffer (__cuda_array_interface__)."""
+
+    def __init__(self, ptr: int, shape):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": "|u1",
+                                         "data": (int(ptr), False), "version": 3}
+
+
+class PeerImage:
+    """Rank 0's image buffer (cudaMalloc on its GPU), mapped into every rank by
+    CUDA IPC (bhrt_ipc_export / bhrt_ipc_open): each rank's kernel stores its
+    rows at their image position in rank 0's HBM over NVLink."""
+
+    def __init__(self, rank: int, device: int, nbytes: int, group=None):
+        L = native.lib()
+        info = StatusInfo()
+        self.rank, self.device, self.ptr = rank, device, C.c_void_p()
+        handle = None
+        if rank == 0:
+            native.check(L.bhrt_device_alloc(device, nbytes, C.byref(self.ptr), C.byref(info)), info)
+            h = (C.c_uint8 * 64)()
+            native.check(L.bhrt_ipc_export(device, self.ptr, h, C.byref(info)), info)
+            handle = bytes(h)
+        obj = [handle]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        if rank != 0:
+            h = (C.c_uint8 * 64).from_buffer_copy(obj[0])
+            native.check(L.bhrt_ipc_open(device, h, C.byref(self.ptr), C.byref(info)), info)
+
+    def tensor(self, shape) -> torch.Tensor:
+        return torch.as_tensor(_DevArray(self.ptr.value, shape), device=f"cuda:{self.device}")
+
+    def close(self):
+        if self.ptr.value:
+            L = native.lib()
+            if self.rank == 0:
+                L.bhrt_device_free(self.device, self.ptr)
+            else:
+                L.bhrt_ipc_close(self.device, self.ptr)
+            self.ptr = C.c_void_p()
 
 
 def rank_rows(height: int, world: int, rank: int, tile_rows: int = 1) -> int:
@@ -51,11 +99,18 @@ class FrameRenderer:
     """
 
     def __init__(self, rank: int = 0, world: int = 1, device: int | None = None,
-                 tile_rows: int = 1, group=None):
+                 tile_rows: int = 1, group=None, peer: bool | None = None):
+        """peer: write rows into rank 0's image over peer memory (default: on
+        for NCCL groups of > 1 rank, falling back to the NCCL gather if the
+        buffer cannot be mapped)."""
         self.rank, self.world, self.tile_rows, self.group = rank, world, tile_rows, group
         self.device = torch.cuda.current_device() if device is None else device
         self.ctx = Context(self.device)
         self._shape = None
+        if peer is None:
+            peer = world > 1 and dist.is_initialized() and dist.get_backend(group) == "nccl"
+        self.want_peer = bool(peer) and world > 1
+        self.peer = None
 
     def _buffers(self, h: int, w: int):
         if self._shape == (h, w):
@@ -70,6 +125,23 @@ class FrameRenderer:
         self.host = torch.empty((h, w, 3), dtype=torch.uint8, pin_memory=True) \
             if self.rank == 0 else None
         self._shape = (h, w)
+        if self.want_peer:
+            if self.peer is not None:
+                self.peer.close()
+            try:
+                self.peer = PeerImage(self.rank, self.device, h * w * 3, self.group)
+                ok = 1
+            except native.BhrtError:
+                self.peer, ok = None, 0
+            # every rank must agree (a rank that cannot map the buffer turns it off)
+            flag = torch.tensor([ok], dtype=torch.int32,
+                                device=f"cuda:{self.device}" if dist.get_backend(self.group) == "nccl"
+                                else "cpu")
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=self.group)
+            if int(flag.item()) == 0 and self.peer is not None:
+                self.peer.close()
+                self.peer = None
+            self.ctx.set_output_layout(1 if self.peer is not None else 0)
 
     def set_scene(self, scene):
         self.ctx.set_scene(scene)
@@ -81,6 +153,18 @@ class FrameRenderer:
         device image on rank 0 (None elsewhere). Scene must be resident."""
         h, w = self.scene.s.height, self.scene.s.width
         st = stream or torch.cuda.current_stream(self.device)
+        if self.peer is not None:
+            # rows go straight into rank 0's image; completion = every rank's
+            # kernel finished (stream-ordered collective after the kernel)
+            self.ctx.render_async(self.peer.ptr.value, 0, h, self.tile_rows, self.world,
+                                  self.rank, stream=st.cuda_stream)
+            if dist.get_backend(self.group) == "nccl":
+                with torch.cuda.stream(st):
+                    dist.all_reduce(self._done_flag(), group=self.group)
+            else:
+                self.ctx.finish()
+                dist.barrier(group=self.group)
+            return self.peer.tensor((h, w, 3)) if self.rank == 0 else None
         self.ctx.render_async(self.out.data_ptr(), 0, h, self.tile_rows, self.world, self.rank,
                               stream=st.cuda_stream)
         if self.world == 1:
@@ -103,8 +187,18 @@ class FrameRenderer:
             dist.gather(self.out, None, dst=0, group=self.group)
         return None
 
+    def _done_flag(self):
+        if getattr(self, "_flag", None) is None:
+            self._flag = torch.zeros(1, dtype=torch.int32, device=f"cuda:{self.device}")
+        return self._flag
+
     def finish(self):
         self.ctx.finish()
+
+    def close(self):
+        if self.peer is not None:
+            self.peer.close()
+            self.peer = None
 
     def render(self, scene, bands: int = 4):  # 4K config 2: 1/2/4/8/16 bands 9.04/8.92/8.85/8.96/9.21 ms
         """End-to-end: H2D scene, render, gather, D2H on rank 0. On one GPU

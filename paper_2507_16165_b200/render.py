@@ -159,6 +159,13 @@ class Context:
                                                 C.c_void_p(stream or 0), C.byref(info))
         _raise(rc, info)
 
+    def set_output_layout(self, image: int):
+        """0: rows packed in order of y (default); 1: d_out is the whole image
+        (bhrt_ctx_set_output_layout)."""
+        rc = native.lib().bhrt_ctx_set_output_layout(self._h, image)
+        if rc:
+            raise native.BhrtError(rc, -1, -1, "bad output layout")
+
     def frame_begin(self, stream: int | None = None):
         """Counters/failures accumulate over the following render_async calls
         (same stream) until finish() (bhrt_ctx_frame_begin)."""

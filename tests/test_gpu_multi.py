@@ -51,36 +51,55 @@ def test_spp_not_dividing_warp_uses_record_path():
     assert d.max() <= 1 and (d > 0).mean() <= 0.001
 
 
-def _rank(rank, world, port, q):
+def _rank(rank, world, port, q, peer=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.cuda.set_device(0)
-    sb = scenes.config(2, 64, 36)
-    fr = parallel.FrameRenderer(rank, world, 0)
-    img = fr.render(sb)
-    if rank == 0:
-        q.put(img.numpy().copy())
+    fr = parallel.FrameRenderer(rank, world, 0, peer=peer)
+    for idx in (2, 1):  # two frames, different sizes: the peer image is re-mapped
+        sb = scenes.config(idx, 64, 36) if idx == 2 else scenes.config(idx, 50, 20)
+        img = fr.render(sb)
+        if rank == 0:
+            q.put((fr.peer is not None, img.numpy().copy()))
+    fr.close()
     dist.barrier()
     dist.destroy_process_group()
 
 
-def test_frame_renderer_two_ranks_share_one_gpu():
-    sb = scenes.config(2, 64, 36)
-    full = render.render_image(sb)
+def _run_ranks(world, peer):
     ctx = mp.get_context("spawn")
     q = ctx.SimpleQueue()
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
     port = s.getsockname()[1]
     s.close()
-    ps = [ctx.Process(target=_rank, args=(r, 2, port, q)) for r in range(2)]
+    ps = [ctx.Process(target=_rank, args=(r, world, port, q, peer)) for r in range(world)]
     for p in ps:
         p.start()
-    img = q.get()
+    out = [q.get(), q.get()]
     for p in ps:
         p.join(300)
         assert p.exitcode == 0
-    assert np.array_equal(img, full)
+    return out
+
+
+def test_frame_renderer_two_ranks_share_one_gpu():
+    (used_peer, a), (_, b) = _run_ranks(2, False)
+    assert not used_peer
+    assert np.array_equal(a, render.render_image(scenes.config(2, 64, 36)))
+    assert np.array_equal(b, render.render_image(scenes.config(1, 50, 20)))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_frame_renderer_peer_image_over_ipc(world):
+    """Each rank's kernel writes its cyclic rows straight into rank 0's image
+    (CUDA IPC mapping, image output layout): no gather, same bytes. The ranks
+    share cuda:0 here (IPC within one device); their kernels never wait on
+    each other — completion is a host barrier after each rank's stream."""
+    (used_peer, a), (_, b) = _run_ranks(world, True)
+    assert used_peer
+    assert np.array_equal(a, render.render_image(scenes.config(2, 64, 36)))
+    assert np.array_equal(b, render.render_image(scenes.config(1, 50, 20)))
 
 
 def test_banded_end_to_end_render_matches_single_launch():
