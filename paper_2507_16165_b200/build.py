@@ -85,7 +85,7 @@ def build_dropin(force: bool = False) -> bool:
     deps = [shim, worker, LIB, os.path.join(ROOT, "include", "bhrt_cuda.h")]
     if not force and all(not _stale(o, deps) for o in outs):
         return True
-    cxx = ["g++", "-std=c++20", "-O2", "-fPIC", "-include", "algorithm", "-I" + os.path.join(REF, "include"),
+    cxx = ["g++", "-std=c++20", "-O2", "-fPIC", "-Wno-free-nonheap-object", "-include", "algorithm", "-I" + os.path.join(REF, "include"),
            "-I" + os.path.join(ROOT, "include")]
     # the reference's sources minus render.cpp (the replaced hot path)
     srcs = [os.path.join(REF, "src", f) for f in sorted(os.listdir(os.path.join(REF, "src")))
