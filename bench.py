@@ -190,6 +190,37 @@ def measure_secondary(device: int, reps: int = 3) -> dict:
                       "Mrays/s": frames * sb0.s.width * sb0.s.height * sb0.s.spp / dt / 1e6,
                       "size": [sb0.s.width, sb0.s.height, sb0.s.spp],
                       "note": "1 GPU; frames shard f mod N across GPUs"}
+    # strong-scaling projection on this one GPU: each rank's cyclic-row share
+    # of the config-2 frame rendered alone (device time), max over ranks, vs
+    # the whole frame / N. Communication is not included (the multi-GPU run
+    # writes rows into rank 0's image over NVLink while they are shaded).
+    sb2 = scenes.config(2)
+    ctx.set_scene(sb2)
+    buf = torch.empty(sb2.s.width * sb2.s.height * 3, dtype=torch.uint8, device="cuda")
+
+    def share_ms(world, rank):
+        best = None
+        for r in range(3):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            ctx.render_async(buf.data_ptr(), 0, sb2.s.height, 1, world, rank, stream=st.cuda_stream)
+            e1.record(st)
+            ctx.finish()
+            ms = e0.elapsed_time(e1)
+            if r > 0 and (best is None or ms < best):
+                best = ms
+        return best
+
+    full = share_ms(1, 0)
+    proj = {"full_frame_ms": full}
+    for world in (2, 4, 8):
+        per = [share_ms(world, r) for r in range(world)]
+        proj[f"n{world}"] = {"max_rank_ms": max(per), "min_rank_ms": min(per),
+                             "efficiency": full / (world * max(per))}
+    proj["note"] = ("device time of each rank's cyclic-row share rendered alone on this GPU; "
+                    "efficiency = T1 / (N * max_rank T_N); excludes the completion collective")
+    out["strong_scaling_projection"] = proj
     # the same orbit written out as PPM files (the host output pipeline,
     # sequence.SequenceRenderer: kernel of frame f overlaps writing f-1)
     import tempfile
