@@ -211,6 +211,13 @@ struct bhrt_ctx {
     unsigned long long* host_stats = nullptr;
     bool in_frame = false;  // bhrt_ctx_frame_begin .. bhrt_ctx_finish: counters accumulate
     int32_t out_image = 0;  // bhrt_ctx_set_output_layout
+    // scene uploads: pinned staging -> device on a private non-blocking stream;
+    // renders wait on up_done, so set_scene does not stall other contexts
+    cudaStream_t up_stream = nullptr;
+    cudaEvent_t up_done = nullptr;
+    cudaEvent_t render_done = nullptr;  // after the last render's counters copy
+    unsigned char* staging = nullptr;
+    size_t staging_cap = 0;
     bool timing = false;
     bool timed = false;
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
@@ -356,6 +363,10 @@ int bhrt_ctx_create(int32_t device, bhrt_ctx** out, bhrt_status_info* info) {
     if (c->stats.ensure(8) || c->queue.ensure(1) || c->tables.ensure(2 * kQN))
         return set_info(info, BHRT_DEVICE, -1, -1, "bhrt_ctx_create: cudaMalloc failed");
     CK(cudaMallocHost(&c->host_stats, 16 * sizeof(unsigned long long)));
+    CK(cudaStreamCreateWithFlags(&c->up_stream, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&c->up_done, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->render_done, cudaEventDisableTiming));
+    CK(cudaEventRecord(c->up_done, c->up_stream));
     for (int i = 0; i < 16; ++i) c->host_stats[i] = 0;
     c->host_stats[3] = c->host_stats[11] = ULLONG_MAX;
     double tb[2 * kQN];
@@ -402,6 +413,10 @@ void bhrt_ctx_destroy(bhrt_ctx* c) {
     c->queue.release();
     c->cull.release();
     if (c->host_stats) cudaFreeHost(c->host_stats);
+    if (c->staging) cudaFreeHost(c->staging);
+    if (c->up_done) cudaEventDestroy(c->up_done);
+    if (c->render_done) cudaEventDestroy(c->render_done);
+    if (c->up_stream) cudaStreamDestroy(c->up_stream);
     c->tab_smp.release();
     c->tab_ends.release();
     c->tab_psi0.release();
@@ -416,7 +431,10 @@ int bhrt_ctx_set_scene(bhrt_ctx* c, const bhrt_scene* s, bhrt_status_info* info)
     rc = validate_trace(s, info);
     if (rc) return rc;
     CK(cudaSetDevice(c->device));
-    CK(cudaDeviceSynchronize());
+    // only this context's own work can still read its buffers: its last
+    // render and its previous uploads (other contexts keep running)
+    if (c->pending) CK(cudaEventSynchronize(c->render_done));
+    CK(cudaStreamSynchronize(c->up_stream));
     KParams& k = c->kp;
     std::memset(&k, 0, sizeof k);
     k.mass = s->mass;
@@ -474,23 +492,41 @@ int bhrt_ctx_set_scene(bhrt_ctx* c, const bhrt_scene* s, bhrt_status_info* info)
     k.n_spheres = s->n_spheres;
     hput(k.light, hnormalized(hv(s->light_dir)));
     k.ambient = s->ambient;
-    if (s->sky_kind == BHRT_SKY_IMAGE) {
-        const size_t bytes = 3ull * s->sky_width * s->sky_height;
-        if (c->sky.ensure(bytes)) return set_info(info, BHRT_DEVICE, -1, -1, "sky alloc failed");
-        CK(cudaMemcpy(c->sky.p, s->sky_rgb, bytes, cudaMemcpyHostToDevice));
+    // host data -> pinned staging -> device (async on the upload stream)
+    const size_t sky_bytes = s->sky_kind == BHRT_SKY_IMAGE ? 3ull * s->sky_width * s->sky_height : 0;
+    const size_t sph_bytes = sizeof(bhrt_sphere) * static_cast<size_t>(s->n_spheres);
+    std::vector<unsigned long long> table;
+    const bool cull = s->n_spheres > 0 && build_cull_table(s, k, table);
+    const size_t cull_bytes = cull ? sizeof(unsigned long long) * table.size() : 0;
+    const size_t need = sky_bytes + sph_bytes + cull_bytes;
+    if (need > c->staging_cap) {
+        if (c->staging) CK(cudaFreeHost(c->staging));
+        c->staging = nullptr;
+        c->staging_cap = 0;
+        CK(cudaMallocHost(&c->staging, need));
+        c->staging_cap = need;
+    }
+    size_t off = 0;
+    if (sky_bytes) {
+        if (c->sky.ensure(sky_bytes)) return set_info(info, BHRT_DEVICE, -1, -1, "sky alloc failed");
+        std::memcpy(c->staging + off, s->sky_rgb, sky_bytes);
+        CK(cudaMemcpyAsync(c->sky.p, c->staging + off, sky_bytes, cudaMemcpyHostToDevice, c->up_stream));
+        off += sky_bytes;
         k.sky = c->sky.p;
         k.sky_w = s->sky_width;
         k.sky_h = s->sky_height;
     }
     if (s->n_spheres > 0) {
         if (c->spheres.ensure(s->n_spheres)) return set_info(info, BHRT_DEVICE, -1, -1, "sphere alloc failed");
-        CK(cudaMemcpy(c->spheres.p, s->spheres, sizeof(bhrt_sphere) * s->n_spheres, cudaMemcpyHostToDevice));
+        std::memcpy(c->staging + off, s->spheres, sph_bytes);
+        CK(cudaMemcpyAsync(c->spheres.p, c->staging + off, sph_bytes, cudaMemcpyHostToDevice, c->up_stream));
+        off += sph_bytes;
         k.spheres = c->spheres.p;
-        std::vector<unsigned long long> table;
-        if (build_cull_table(s, k, table)) {
+        if (cull) {
             if (c->cull.ensure(table.size())) return set_info(info, BHRT_DEVICE, -1, -1, "cull alloc failed");
-            CK(cudaMemcpy(c->cull.p, table.data(), sizeof(unsigned long long) * table.size(),
-                          cudaMemcpyHostToDevice));
+            std::memcpy(c->staging + off, table.data(), cull_bytes);
+            CK(cudaMemcpyAsync(c->cull.p, c->staging + off, cull_bytes, cudaMemcpyHostToDevice, c->up_stream));
+            off += cull_bytes;
             k.cull = c->cull.p;
         }
     }
@@ -511,9 +547,9 @@ int bhrt_ctx_set_scene(bhrt_ctx* c, const bhrt_scene* s, bhrt_status_info* info)
             if (c->tab_smp.ensure(E * s->table_samples * 2) || c->tab_ends.ensure(E * 4) ||
                 c->tab_kind.ensure(E) || c->tab_n.ensure(E) || c->tab_psi0.ensure(E))
                 return set_info(info, BHRT_DEVICE, -1, -1, "table alloc failed");
-            launch_table_build(k, c->tab_smp.p, c->tab_ends.p, c->tab_kind.p, c->tab_n.p, nullptr);
+            launch_table_build(k, c->tab_smp.p, c->tab_ends.p, c->tab_kind.p, c->tab_n.p, c->up_stream);
             CK(cudaGetLastError());
-            CK(cudaDeviceSynchronize());
+            CK(cudaStreamSynchronize(c->up_stream));
             std::memcpy(c->table_key, key, sizeof key);
             c->has_table = true;
         }
@@ -524,12 +560,12 @@ int bhrt_ctx_set_scene(bhrt_ctx* c, const bhrt_scene* s, bhrt_status_info* info)
         k.tab_psi0 = c->tab_psi0.p;
         // bind the frame: each entry's inbound psi of the camera's u0 (oracle prep_table)
         const double u0 = 1.0 / hnorm(hsub(hv(s->cam_pos), hv(s->center)));
-        launch_table_bind(k, c->tab_ends.p, c->tab_psi0.p, u0, nullptr);
+        launch_table_bind(k, c->tab_ends.p, c->tab_psi0.p, u0, c->up_stream);
         CK(cudaGetLastError());
-        CK(cudaDeviceSynchronize());
     }
     k.grow = c->tables.p;
     k.shrink = c->tables.p + kQN;
+    CK(cudaEventRecord(c->up_done, c->up_stream));  // renders wait on this
     c->scene = *s;
     c->has_scene = true;
     return 0;
@@ -563,6 +599,7 @@ int bhrt_ctx_render_async(bhrt_ctx* c, int32_t row_start, int32_t row_end, int32
     k.out_image = c->out_image;
     k.stats = c->stats.p;
     k.queue = c->queue.p;
+    CK(cudaStreamWaitEvent(st, c->up_done, 0));  // the scene's uploads
     if (!c->in_frame) {  // counters + lowest failing pixel start fresh for this render
         CK(cudaMemcpyAsync(c->stats.p, c->host_stats + 8, 8 * sizeof(unsigned long long),
                            cudaMemcpyHostToDevice, st));
@@ -575,6 +612,7 @@ int bhrt_ctx_render_async(bhrt_ctx* c, int32_t row_start, int32_t row_end, int32
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(c->host_stats, c->stats.p, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                        st));
+    CK(cudaEventRecord(c->render_done, st));
     c->last_stream = st;
     c->pending = 1;
     c->last_rows = rows;
@@ -652,7 +690,7 @@ int bhrt_ctx_finish(bhrt_ctx* c, bhrt_status_info* info) {
     CK(cudaSetDevice(c->device));
     c->in_frame = false;
     if (!c->pending) return 0;
-    CK(cudaStreamSynchronize(c->last_stream));
+    CK(cudaEventSynchronize(c->render_done));  // this render only, not later work on the stream
     c->pending = 0;
     const unsigned long long fail = c->host_stats[3];  // lowest failing y * width + x
     if (fail != ULLONG_MAX) {
