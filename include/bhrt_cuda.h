@@ -246,9 +246,11 @@ int bhrt_ctx_render_async(bhrt_ctx* ctx, int32_t row_start, int32_t row_end, int
 /* Opens a frame of several render_async calls (e.g. row bands enqueued back
  * to back so each band's copy-out overlaps the next band's kernel): counters
  * and the lowest failing pixel are reset once here on `stream` and then
- * accumulate over the frame's render_async calls (issue them on the same
- * stream) until bhrt_ctx_finish, which reports the lowest failing pixel of
- * the whole frame. Without it every render_async starts fresh. */
+ * accumulate over the frame's render_async calls — which may be issued on
+ * different streams (e.g. alternating, so one band's kernel fills the SMs
+ * while the previous band's last blocks finish) — until bhrt_ctx_finish,
+ * which waits for all of them and reports the lowest failing pixel of the
+ * whole frame. Without it every render_async starts fresh. */
 int bhrt_ctx_frame_begin(bhrt_ctx* ctx, void* stream, bhrt_status_info* info);
 /* Waits for the context's last render on its stream and reports the lowest
  * failing pixel, if any. */

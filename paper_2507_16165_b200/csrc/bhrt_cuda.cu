@@ -216,6 +216,8 @@ struct bhrt_ctx {
     cudaStream_t up_stream = nullptr;
     cudaEvent_t up_done = nullptr;
     cudaEvent_t render_done = nullptr;  // after the last render's counters copy
+    std::vector<cudaEvent_t> frame_ev;  // one per render of the open frame (any streams)
+    size_t frame_nev = 0;
     unsigned char* staging = nullptr;
     size_t staging_cap = 0;
     bool timing = false;
@@ -416,6 +418,7 @@ void bhrt_ctx_destroy(bhrt_ctx* c) {
     if (c->staging) cudaFreeHost(c->staging);
     if (c->up_done) cudaEventDestroy(c->up_done);
     if (c->render_done) cudaEventDestroy(c->render_done);
+    for (auto e : c->frame_ev) cudaEventDestroy(e);
     if (c->up_stream) cudaStreamDestroy(c->up_stream);
     c->tab_smp.release();
     c->tab_ends.release();
@@ -610,9 +613,20 @@ int bhrt_ctx_render_async(bhrt_ctx* c, int32_t row_start, int32_t row_end, int32
     if (rows > 0 && launch_trace(k, st, &c->launches, c->timed ? c->ev : nullptr) != 0)
         return set_info(info, BHRT_INVALID_ARGUMENT, -1, -1, "render: unsupported integrator");
     CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(c->host_stats, c->stats.p, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                       st));
-    CK(cudaEventRecord(c->render_done, st));
+    if (c->in_frame) {
+        // counters accumulate on the device; finish() reads them once after
+        // every render of the frame (its renders may run on several streams)
+        if (c->frame_nev == c->frame_ev.size()) {
+            cudaEvent_t e;
+            CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            c->frame_ev.push_back(e);
+        }
+        CK(cudaEventRecord(c->frame_ev[c->frame_nev++], st));
+    } else {
+        CK(cudaMemcpyAsync(c->host_stats, c->stats.p, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                           st));
+        CK(cudaEventRecord(c->render_done, st));
+    }
     c->last_stream = st;
     c->pending = 1;
     c->last_rows = rows;
@@ -681,6 +695,7 @@ int bhrt_ctx_frame_begin(bhrt_ctx* c, void* stream, bhrt_status_info* info) {
                        st));
     c->launches = 0;
     c->in_frame = true;
+    c->frame_nev = 0;
     return 0;
 }
 
@@ -688,6 +703,14 @@ int bhrt_ctx_finish(bhrt_ctx* c, bhrt_status_info* info) {
     set_info(info, 0, -1, -1, "");
     if (!c) return set_info(info, BHRT_INVALID_ARGUMENT, -1, -1, "NULL context");
     CK(cudaSetDevice(c->device));
+    if (c->in_frame && c->pending) {
+        for (size_t i = 0; i < c->frame_nev; ++i) CK(cudaEventSynchronize(c->frame_ev[i]));
+        CK(cudaMemcpyAsync(c->host_stats, c->stats.p, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                           c->up_stream));
+        CK(cudaStreamSynchronize(c->up_stream));
+        CK(cudaEventRecord(c->render_done, c->up_stream));
+    }
+    c->frame_nev = 0;
     c->in_frame = false;
     if (!c->pending) return 0;
     CK(cudaEventSynchronize(c->render_done));  // this render only, not later work on the stream
