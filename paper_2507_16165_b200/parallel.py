@@ -221,11 +221,11 @@ class FrameRenderer:
         if getattr(self, "_copy_stream", None) is None:
             self._copy_stream = torch.cuda.Stream(self.device)
         cs = self._copy_stream
-        if getattr(self, "_band_streams", None) is None:
-            # bands alternate between two streams: band b+1's kernel starts
-            # while band b's last (longest) blocks still run
-            self._band_streams = [st, torch.cuda.Stream(self.device)]
-        streams = self._band_streams
+        if getattr(self, "_band_stream", None) is None:
+            self._band_stream = torch.cuda.Stream(self.device)
+        # bands alternate between the caller's stream and a second one: band
+        # b+1's kernel starts while band b's last (longest) blocks still run
+        streams = [st, self._band_stream]
         out = self.out.view(-1)
         host = self.host.view(-1)
         row_bytes = 3 * w
