@@ -69,7 +69,9 @@ __device__ __forceinline__ float atan2_cull(float y, float x) {
     return copysignf(r, y);
 }
 
-__device__ __forceinline__ void sphere_window_f(double cx, double cy, double rho2, float& lo, float& hi) {
+// rcf = |(cx, cy)| and rhof = sqrt(rho2) in fp32 (shared with the radial extent)
+__device__ __forceinline__ void sphere_window_f(double cx, double cy, double rho2, float rcf, float rhof,
+                                                float& lo, float& hi) {
     const double q = cx * cx + cy * cy - rho2;  // rc^2 - rho^2
     if (!(q > 0.0)) {
         lo = -CUDART_INF_F;
@@ -79,8 +81,7 @@ __device__ __forceinline__ void sphere_window_f(double cx, double cy, double rho
     // half-width asin(x), x = rho/rc, bounded from above without a second
     // atan2: asin(x) <= x (1 + x^2/5) on [0, 1/2] (series 1/6 + 3x^2/40 + ...),
     // and <= pi/2 beyond.
-    const float rcf = sqrtf((float)(cx * cx + cy * cy));
-    const float x = sqrtf((float)rho2) / rcf;
+    const float x = __fdividef(rhof, rcf);  // culling only: ~2 ulp is far inside the margins
     const float a = x <= 0.5f ? x * (1.0f + 0.2f * x * x) * 1.0001f : 1.5708f;
     (void)q;
     const float pc = atan2_cull((float)cy, (float)cx);
@@ -123,11 +124,11 @@ __device__ double events_setup(const KParams& p, SceneSm& sm, int t, V3 e1, V3 e
         }
         const double cx = dot(c, e1), cy = dot(c, e2);
         const double rho2 = r * r - dn * dn;
+        const float rc = sqrtf((float)(cx * cx + cy * cy)), rho = sqrtf((float)rho2);
         float lo, hi;
-        sphere_window_f(cx, cy, rho2, lo, hi);
+        sphere_window_f(cx, cy, rho2, rc, rho, lo, hi);
         sm.lo[nc][t] = lo;
         sm.hi[nc][t] = hi;
-        const float rc = sqrtf((float)(cx * cx + cy * cy)), rho = sqrtf((float)rho2);
         sm.rlo[nc][t] = (rc - rho) - 1e-5f * (rc + rho);  // fp32 rounding << 1e-5
         sm.rhi[nc][t] = (rc + rho) * (1.0f + 1e-5f);
         sm.k[nc][t] = (unsigned char)k;
