@@ -233,6 +233,9 @@ __device__ static __noinline__ void sample_direction(const KParams& p, V3 d, dou
 #ifndef BHRT_INL_SPH
 #define BHRT_INL_SPH __noinline__
 #endif
+#ifndef BHRT_INL_SETUP
+#define BHRT_INL_SETUP  // compiler's choice (single call site)
+#endif
 __device__ static BHRT_INL_SHADE void shade_sample(const KParams& p, int obj, int sphere, V3 pt, double rgb[3]) {
     rgb[0] = rgb[1] = rgb[2] = 0.0;
     if (obj == BHRT_OBJ_SKY) {

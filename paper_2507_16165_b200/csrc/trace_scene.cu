@@ -95,7 +95,7 @@ __device__ __forceinline__ void sphere_window_f(double cx, double cy, double rho
 
 // Disk line + sphere candidates (oracle ray_events_setup). Returns the first
 // event angle.
-__device__ double events_setup(const KParams& p, SceneSm& sm, int t, V3 e1, V3 e2, V3 n) {
+__device__ BHRT_INL_SETUP double events_setup(const KParams& p, SceneSm& sm, int t, V3 e1, V3 e2, V3 n) {
     double next_disk = CUDART_INF;
     sm.sigma[t] = 1.0;
     if (p.disk_enabled) {
