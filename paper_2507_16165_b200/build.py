@@ -35,15 +35,23 @@ def _stale(target: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
+DEBUG_LIB = os.path.join(PKG, "libbhrt_b200_debug.so")
+
+
+def build(verbose: bool = False, force: bool = False, debug: bool = False) -> str:
+    """libbhrt_b200.so; debug=True: libbhrt_b200_debug.so with device bounds
+    checks (-DBHRT_DEBUG_BOUNDS), loaded by tests/test_gpu_debug_bounds.py."""
+    target = DEBUG_LIB if debug else LIB
+    flags = NVFLAGS + (["-DBHRT_DEBUG_BOUNDS"] if debug else [])
+    tag = "_debug" if debug else ""
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
     deps.append(os.path.join(ROOT, "include", "bhrt_cuda.h"))
-    if force or _stale(LIB, deps):
+    if force or _stale(target, deps):
         objs = []
         os.makedirs(os.path.join(ROOT, "build"), exist_ok=True)
         for src in SOURCES:
-            obj = os.path.join(ROOT, "build", os.path.splitext(src)[0] + ".o")
-            cmd = [NVCC, *ARCH, *NVFLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+            obj = os.path.join(ROOT, "build", os.path.splitext(src)[0] + tag + ".o")
+            cmd = [NVCC, *ARCH, *flags, "-c", os.path.join(CSRC, src), "-o", obj]
             r = subprocess.run(cmd, capture_output=True, text=True)
             if r.returncode != 0:
                 sys.stderr.write(r.stdout + r.stderr)
@@ -51,14 +59,14 @@ def build(verbose: bool = False, force: bool = False) -> str:
             if verbose:
                 sys.stderr.write(r.stderr)
             objs.append(obj)
-        tmp = LIB + ".tmp"
+        tmp = target + ".tmp"
         cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError("link failed")
-        os.replace(tmp, LIB)
-    return LIB
+        os.replace(tmp, target)
+    return target
 
 
 REF = "/root/reference/proj"
@@ -107,6 +115,7 @@ def build_oracle() -> None:
 
 if __name__ == "__main__":
     build(verbose=True, force="--force" in sys.argv)
+    build(force="--force" in sys.argv, debug=True)
     build_dropin(force="--force" in sys.argv)
     build_oracle()
     print(LIB)

@@ -13,6 +13,16 @@
 
 #include "bhrt_kernel_params.h"
 
+// Device bounds checks of the debug build (libbhrt_b200_debug.so,
+// -DBHRT_DEBUG_BOUNDS; compute-sanitizer is not available on the GPU pool):
+// a failed check traps the kernel and the render reports BHRT_DEVICE.
+#ifdef BHRT_DEBUG_BOUNDS
+#include <cassert>
+#define BHRT_ASSERT(c) assert(c)
+#else
+#define BHRT_ASSERT(c) ((void)0)
+#endif
+
 namespace bhrt_b200 {
 
 #define PI_D 3.141592653589793
@@ -314,6 +324,7 @@ __device__ __forceinline__ void finish_sample(const KParams& p, bool valid, cons
     const bool has_point = obj == BHRT_OBJ_SKY || obj == BHRT_OBJ_DISK || obj == BHRT_OBJ_SPHERE;
     if (valid && p.records) {
         bhrt_ray_record rec;
+        BHRT_ASSERT(id.rec >= 0 && id.rec < (long long)p.n_rows * p.width * p.spp);
         rec.object = obj;
         rec.sphere = sphere;
         rec.steps = (int)steps;
@@ -349,6 +360,8 @@ __device__ __forceinline__ void finish_sample(const KParams& p, bool valid, cons
     }
     if (valid && id.s == 0) {
         const long long pix = id.rec / p.spp;
+        BHRT_ASSERT(id.x >= 0 && id.x < p.width && id.y >= p.row_start && id.y < p.row_end &&
+                    pix >= 0 && pix < (long long)p.n_rows * p.width);
         uint8_t* o = p.out + 3 * (p.out_image ? (long long)id.y * p.width + id.x : pix);
         if (anybad) {
             atomicMin(&p.stats[3], (unsigned long long)id.y * p.width + id.x);  // image order
@@ -443,6 +456,7 @@ __device__ __forceinline__ bool rkf45_step(double u, double w, double h, double 
     const int dw_ = __double2hiint(ew) - __double2hiint(dw);
     int q = (du_ > dw_ ? du_ : dw_) >> 18;
     q = q < kQMin ? kQMin : (q > kQMin + kQN - 1 ? kQMin + kQN - 1 : q);
+    BHRT_ASSERT(q - kQMin >= 0 && q - kQMin < kQN);
     if (err_ok && geo_ok) {
         un = u_new;
         wn = w_new;

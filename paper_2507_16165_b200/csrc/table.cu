@@ -296,6 +296,7 @@ __global__ void __launch_bounds__(128) trace_table_kernel(const __grid_constant_
                 const double x = (b * (double)(N - 1)) / p.table_b_max;
                 int ie = (int)floor(x);
                 if (ie > N - 2) ie = N - 2;
+                BHRT_ASSERT(ie >= 0 && ie + 1 < N);
                 double f = x - (double)ie;
                 if (__ldg(&p.tab_kind[ie]) == 3) f = 1.0;
                 const double p0i = __ldg(&p.tab_psi0[ie]), p0j = __ldg(&p.tab_psi0[ie + 1]);

@@ -131,6 +131,7 @@ __device__ BHRT_INL_SETUP double events_setup(const KParams& p, SceneSm& sm, int
         sm.hi[nc][t] = hi;
         sm.rlo[nc][t] = (rc - rho) - 1e-5f * (rc + rho);  // fp32 rounding << 1e-5
         sm.rhi[nc][t] = (rc + rho) * (1.0f + 1e-5f);
+        BHRT_ASSERT(k >= 0 && k < p.n_spheres && nc >= 0 && nc < kSlots);
         sm.k[nc][t] = (unsigned char)k;
         next_sph = fminf(next_sph, lo);
         ++nc;
@@ -236,6 +237,7 @@ __device__ BHRT_INL_SPH bool sphere_search(const KParams& p, const SceneSm& sm, 
         } else {
             if (!(act & (1u << a))) continue;
             k = sm.k[a][t];
+            BHRT_ASSERT(k < p.n_spheres);
             // clamp in float first: windows may be infinite
             const float fS = (float)S;
             j0 = (int)fminf(fmaxf(floorf((sm.lo[a][t] - fpa) * rdl) - 1.0f, 0.0f), fS);

@@ -26,4 +26,4 @@ d /= np.linalg.norm(d, axis=1)[:, None]
 G.trace_batch(o, d, G.BlackHole(1.0), G.TraceConfig(epsilon=0.2, escape_radius=100.0), deflection=True)
 fr = parallel.FrameRenderer()
 fr.render(scenes.config(2, 32, 18), bands=4)
-print("sanitize run done")
+print("all paths done")
