@@ -450,6 +450,7 @@ def run_ours(args):
         "reference_sky_only": ref_sky,
         "e2e": {"value": e2e_value, "unit": "Mrays/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
+        "mpixels_per_s": value / spp,  # BASELINE metric also quotes pixels/s
         "gpu_launches": stats["launches"] * args.steps if stats else None,
         "gpu_launches_per_step": stats["launches"] if stats else None,
         "steps_per_ray": stats["steps"] / stats["rays"] if stats else None,
