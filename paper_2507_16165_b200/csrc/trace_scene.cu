@@ -29,7 +29,6 @@ constexpr float kWinMargin = 5e-4f;  // fp32 window slack (rad); windows only cu
 
 struct SceneSm {
     float4 sph[kSphSm];  // (cx, cy, cz, r + fp32 slack) relative to the hole: cull prefilter
-    double grow[kQN], shrink[kQN];
     double e1[3][kBlock], e2[3][kBlock], n[3][kBlock];
     double sigma[kBlock], energy[kBlock], next_disk[kBlock];
     float lo[kSlots][kBlock], hi[kSlots][kBlock];   // angular window (unwrapped phi)
@@ -525,12 +524,7 @@ __global__ void __launch_bounds__(kBlock, BHRT_SCENE_MINB)
         const float slack = 1e-5f * (float)(norm(c) + r) + 1e-6f;
         sm.sph[k] = make_float4((float)c.x, (float)c.y, (float)c.z, (float)r + slack);
     }
-    if (INTEG == BHRT_INTEGRATOR_RKF45)
-        for (int k = t; k < kQN; k += blockDim.x) {
-            sm.grow[k] = p.grow[k];
-            sm.shrink[k] = p.shrink[k];
-        }
-    __syncthreads();
+    if (!p.cull) __syncthreads();  // uniform over the grid (kernel parameter)
 
     const long long n = (long long)p.n_rows * p.width * p.spp;
 #if BHRT_SCENE_PERSISTENT
@@ -605,7 +599,9 @@ __global__ void __launch_bounds__(kBlock, BHRT_SCENE_MINB)
                     if (u <= p.u_esc && w < 0.0) { H.obj = BHRT_OBJ_SKY; break; }
                     if (phi > p.phi_max) { H.obj = BHRT_OBJ_STALLED; break; }
                     double un, wn, hn;
-                    if (rkf45_step(u, w, h, p.M3, p.rel_tol, p.abs_tol, p.max_step, sm.grow, sm.shrink, un,
+                    // controller factors straight from the (L1-resident) global tables: measured
+                    // faster than staging them in shared memory (8.21 -> 8.05 ms, config 2)
+                    if (rkf45_step(u, w, h, p.M3, p.rel_tol, p.abs_tol, p.max_step, p.grow, p.shrink, un,
                                    wn, hn)) {
                         const double pn = phi + h;
                         ++nsteps;
