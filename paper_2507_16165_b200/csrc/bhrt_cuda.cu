@@ -195,6 +195,7 @@ struct bhrt_ctx {
     DevBuf<double> tables;
     DevBuf<bhrt_ray_record> records;
     DevBuf<double> rays, defl;  // bhrt_cuda_trace_rays
+    DevBuf<double> checker;     // checker cell boundaries (KParams::checker_tab)
     DevBuf<uint8_t> out;
     DevBuf<unsigned long long> stats;
     DevBuf<unsigned int> queue;
@@ -414,6 +415,9 @@ void bhrt_ctx_destroy(bhrt_ctx* c) {
     c->stats.release();
     c->queue.release();
     c->cull.release();
+    c->checker.release();
+    c->rays.release();
+    c->defl.release();
     if (c->host_stats) cudaFreeHost(c->host_stats);
     if (c->staging) cudaFreeHost(c->staging);
     if (c->up_done) cudaEventDestroy(c->up_done);
@@ -479,11 +483,12 @@ int bhrt_ctx_set_scene(bhrt_ctx* c, const bhrt_scene* s, bhrt_status_info* info)
     k.sky_kind = s->sky_kind;
     k.checker_nu = s->checker_nu;
     k.checker_nv = s->checker_nv;
-    for (int i = 0; i < kCheckerMax; ++i) {  // checker cell boundaries (shade_sample)
+    double checker[3 * kCheckerMax];  // cell boundaries (shade_sample), uploaded below
+    for (int i = 0; i < kCheckerMax; ++i) {
         const double th = -kPi + 2.0 * kPi * i / (s->checker_nu > 0 ? s->checker_nu : 1);
-        k.checker_uc[i] = std::cos(th);
-        k.checker_us[i] = std::sin(th);
-        k.checker_vc[i] = std::cos(kPi * i / (s->checker_nv > 0 ? s->checker_nv : 1));
+        checker[i] = std::cos(th);
+        checker[kCheckerMax + i] = std::sin(th);
+        checker[2 * kCheckerMax + i] = std::cos(kPi * i / (s->checker_nv > 0 ? s->checker_nv : 1));
     }
     std::memcpy(k.checker_a, s->checker_color_a, sizeof k.checker_a);
     std::memcpy(k.checker_b, s->checker_color_b, sizeof k.checker_b);
@@ -501,7 +506,8 @@ int bhrt_ctx_set_scene(bhrt_ctx* c, const bhrt_scene* s, bhrt_status_info* info)
     std::vector<unsigned long long> table;
     const bool cull = s->n_spheres > 0 && build_cull_table(s, k, table);
     const size_t cull_bytes = cull ? sizeof(unsigned long long) * table.size() : 0;
-    const size_t need = sky_bytes + sph_bytes + cull_bytes;
+    const size_t chk_bytes = sizeof checker;
+    const size_t need = chk_bytes + sky_bytes + sph_bytes + cull_bytes;
     if (need > c->staging_cap) {
         if (c->staging) CK(cudaFreeHost(c->staging));
         c->staging = nullptr;
@@ -510,6 +516,11 @@ int bhrt_ctx_set_scene(bhrt_ctx* c, const bhrt_scene* s, bhrt_status_info* info)
         c->staging_cap = need;
     }
     size_t off = 0;
+    if (c->checker.ensure(3 * kCheckerMax)) return set_info(info, BHRT_DEVICE, -1, -1, "checker alloc failed");
+    std::memcpy(c->staging + off, checker, chk_bytes);
+    CK(cudaMemcpyAsync(c->checker.p, c->staging + off, chk_bytes, cudaMemcpyHostToDevice, c->up_stream));
+    off += chk_bytes;
+    k.checker_tab = c->checker.p;
     if (sky_bytes) {
         if (c->sky.ensure(sky_bytes)) return set_info(info, BHRT_DEVICE, -1, -1, "sky alloc failed");
         std::memcpy(c->staging + off, s->sky_rgb, sky_bytes);

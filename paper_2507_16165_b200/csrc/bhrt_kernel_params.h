@@ -47,9 +47,11 @@ struct KParams {
     int32_t pad1;
     const uint8_t* sky;
     double checker_a[3], checker_b[3];
-    // cell boundaries: longitude k at atan2 = -pi + 2 pi k / nu as (cos, sin);
-    // latitude k at y = cos(pi k / nv)
-    double checker_uc[kCheckerMax], checker_us[kCheckerMax], checker_vc[kCheckerMax];
+    // cell boundaries (device array, 3 x kCheckerMax): longitude k at
+    // atan2 = -pi + 2 pi k / nu as cos [k], sin [kCheckerMax + k]; latitude k
+    // at y = cos(pi k / nv) [2 kCheckerMax + k]. In global memory, not in the
+    // parameter bank: the per-lane binary search indexes it divergently.
+    const double* checker_tab;
     // disk
     int32_t disk_enabled;
     int32_t n_spheres;

@@ -259,7 +259,7 @@ __device__ static BHRT_INL_SHADE void shade_sample(const KParams& p, int obj, in
                 int lo = 0, hi = p.checker_nu;      // count in [lo, hi)
                 while (hi - lo > 1) {
                     const int k = (lo + hi) >> 1;
-                    const double ck = p.checker_uc[k], sk = p.checker_us[k];
+                    const double ck = __ldg(p.checker_tab + k), sk = __ldg(p.checker_tab + kCheckerMax + k);
                     const bool kup = sk > 0.0 || (sk == 0.0 && ck > 0.0);
                     const bool ge = upper != kup ? upper : (ck * pt.z - sk * pt.x >= 0.0);
                     if (ge) lo = k; else hi = k;
@@ -270,7 +270,7 @@ __device__ static BHRT_INL_SHADE void shade_sample(const KParams& p, int obj, in
                 const double y = clampd(pt.y, -1.0, 1.0);
                 while (hi - lo > 1) {
                     const int k = (lo + hi) >> 1;
-                    if (y <= p.checker_vc[k]) lo = k; else hi = k;
+                    if (y <= __ldg(p.checker_tab + 2 * kCheckerMax + k)) lo = k; else hi = k;
                 }
                 cv = lo;
             } else {
