@@ -98,6 +98,7 @@ struct KParams {
 };
 
 __host__ __device__ inline int packed_row_to_y(const KParams& p, int j) {
+    if (p.tile_rows == 1) return p.row_start + j * p.tile_stride + p.tile_offset;  // no division
     const int tile = j / p.tile_rows;
     const int within = j - tile * p.tile_rows;
     return p.row_start + (tile * p.tile_stride + p.tile_offset) * p.tile_rows + within;

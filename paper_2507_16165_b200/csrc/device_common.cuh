@@ -359,7 +359,7 @@ __device__ __forceinline__ void finish_sample(const KParams& p, bool valid, cons
         anybad |= __shfl_sync(0xffffffffu, bad, base + q);
     }
     if (valid && id.s == 0) {
-        const long long pix = id.rec / p.spp;
+        const long long pix = id.rec >> (__ffs(p.spp) - 1);  // fused: spp is a power of two
         BHRT_ASSERT(id.x >= 0 && id.x < p.width && id.y >= p.row_start && id.y < p.row_end &&
                     pix >= 0 && pix < (long long)p.n_rows * p.width);
         uint8_t* o = p.out + 3 * (p.out_image ? (long long)id.y * p.width + id.x : pix);
