@@ -242,7 +242,10 @@ __device__ __forceinline__ RResult window_loop(const KParams& p, V3 origin, V3 c
     return R;
 }
 
-__global__ void __launch_bounds__(128) trace_reference_kernel(const __grid_constant__ KParams p) {
+#ifndef BHRT_REF_MINB
+#define BHRT_REF_MINB 8  // 64 regs, 32 warps/SM: 1/4/6/7/8/10 blocks -> 31.7/31.8/28.6/28.5/28.3/29.4 ms (960x540 mode R)
+#endif
+__global__ void __launch_bounds__(128, BHRT_REF_MINB) trace_reference_kernel(const __grid_constant__ KParams p) {
     const long long n = (long long)p.n_rows * p.width * p.spp;
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     unsigned nsteps = 0, nrej = 0;
@@ -279,7 +282,7 @@ __global__ void __launch_bounds__(128) trace_reference_kernel(const __grid_const
 // orc_initial_conditions, same operations). Origins inside the horizon are
 // rejected on the host before launch.
 template <bool DEFL>
-__global__ void __launch_bounds__(128) trace_rays_kernel(const __grid_constant__ KParams p, const double* rays,
+__global__ void __launch_bounds__(128, BHRT_REF_MINB) trace_rays_kernel(const __grid_constant__ KParams p, const double* rays,
                                                          long long n, bhrt_ray_record* records, double* defl) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
