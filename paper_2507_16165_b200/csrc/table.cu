@@ -237,7 +237,10 @@ __device__ __forceinline__ bool table_plan(const TabView& T, int e, double psi0,
     return true;
 }
 
-__global__ void __launch_bounds__(128) trace_table_kernel(const __grid_constant__ KParams p) {
+#ifndef BHRT_TAB_MINB
+#define BHRT_TAB_MINB 6  // 1/6/8/10 blocks -> 2.36/2.34/2.41/2.54 ms (config 3)
+#endif
+__global__ void __launch_bounds__(128, BHRT_TAB_MINB) trace_table_kernel(const __grid_constant__ KParams p) {
     const long long n = (long long)p.n_rows * p.width * p.spp;
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const bool valid = i < n;
