@@ -260,7 +260,7 @@ int bhrt_ctx_finish(bhrt_ctx* ctx, bhrt_status_info* info);
 int bhrt_ctx_stats(bhrt_ctx* ctx, uint64_t* steps, uint64_t* rejected, uint64_t* rays,
                    int32_t* launches);
 /* Raw device counters of the last finished render: [0] steps, [1] rejected,
- * [2] rays, [3] lowest failing packed pixel (UINT64_MAX: none), [4..7]
+ * [2] rays, [3] lowest failing pixel as y * width + x (UINT64_MAX: none), [4..7]
  * diagnostic counters of builds with -DBHRT_COUNTERS (0 otherwise). */
 int bhrt_ctx_counters(bhrt_ctx* ctx, uint64_t out[8]);
 /* Per-kernel CUDA-event timing of subsequent renders (off by default).

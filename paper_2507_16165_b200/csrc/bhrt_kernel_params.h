@@ -93,7 +93,7 @@ struct KParams {
     // outputs
     bhrt_ray_record* records;   // n_rows * width * spp
     uint8_t* out;               // n_rows * width * 3
-    unsigned long long* stats;  // [0] steps, [1] rejected, [2] rays, [3] lowest failing index+1
+    unsigned long long* stats;  // [0] steps, [1] rejected, [2] rays, [3] lowest failing y*width+x (ULLONG_MAX: none), [4..7] BHRT_COUNTERS
     unsigned int* queue;        // persistent work counter
 };
 
