@@ -1,0 +1,37 @@
+"""bench.py's reference arm runs without a GPU (CPU oracle port): its JSON
+line carries the driver contract's keys (impl, metric/unit, cpu_baseline
+with kind/cores/sample, e2e with zero copy bytes), and under torchrun only
+rank 0 prints."""
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def run(args, env=None):
+    e = dict(os.environ, **(env or {}))
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *args], cwd=ROOT, env=e,
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    return [json.loads(line) for line in r.stdout.splitlines() if line.startswith("{")]
+
+
+def test_reference_arm_line():
+    lines = run(["--impl", "reference", "--steps", "2", "--warmup", "1", "--ref-rows", "4"])
+    assert len(lines) == 1
+    d = lines[0]
+    assert d["impl"] == "reference" and d["metric"] == "Mrays/s" and d["unit"] == "Mrays/s"
+    assert d["higher_is_better"] is True and d["steps"] == 2 and d["warmup"] == 1
+    assert d["value"] > 0 and d["cpu_baseline"]["value"] == d["value"]
+    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
+    assert "sample" in d["cpu_baseline"]
+    assert d["e2e"] == {"value": d["value"], "unit": "Mrays/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}
+    assert d["config"]["workload"].startswith("config2")
+
+
+def test_reference_arm_only_rank0_prints():
+    assert run(["--impl", "reference", "--steps", "1", "--warmup", "0", "--ref-rows", "2"],
+               env={"RANK": "1", "WORLD_SIZE": "2", "LOCAL_RANK": "1"}) == []
