@@ -794,6 +794,11 @@ extern "C" int bhrt_cuda_render_rows(const bhrt_scene* s, int32_t row_start, int
         devs.push_back(d);
     } else {
         devs.assign(devices, devices + ndev);
+        for (int i = 0; i < ndev; ++i) {  // one cached context per device: each device once
+            bool bad = devs[i] < 0;
+            for (int j = 0; j < i; ++j) bad = bad || devs[i] == devs[j];
+            if (bad) return set_info(info, BHRT_INVALID_ARGUMENT, -1, -1, "render: duplicate or negative device");
+        }
     }
     const int G = static_cast<int>(devs.size());
     const int tile_rows = 1;  // cyclic rows (7.78x vs 6.35x for bands)

@@ -161,3 +161,11 @@ def test_trace_rays_host_validation_without_gpu():
     assert len(rec) == 0 and len(defl) == 0
     with pytest.raises(G.InvalidArgument, match="deflection_angle"):
         G.deflection_angle(0.0)
+
+
+def test_render_rows_rejects_duplicate_devices_without_gpu():
+    from paper_2507_16165_b200 import render
+    sb = scenes.config(1, 16, 8)
+    for devs in ([0, 0], [1, -1]):
+        with pytest.raises(render.InvalidArgument, match="device"):
+            render.render_rows(sb, 0, 1, devices=devs)
