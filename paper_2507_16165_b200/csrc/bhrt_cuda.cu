@@ -594,6 +594,7 @@ int bhrt_ctx_render_async(bhrt_ctx* c, int32_t row_start, int32_t row_end, int32
         return set_info(info, BHRT_INVALID_ARGUMENT, -1, -1, "render: row range out of bounds");
     const int32_t rows = bhrt_tile_row_count(row_start, row_end, tile_rows, tile_stride, tile_offset);
     if (rows < 0) return set_info(info, BHRT_INVALID_ARGUMENT, -1, -1, "render: bad tiling");
+    if (rows > 0 && d_out == nullptr) return set_info(info, BHRT_INVALID_ARGUMENT, -1, -1, "render: NULL output");
     CK(cudaSetDevice(c->device));
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     KParams k = c->kp;
