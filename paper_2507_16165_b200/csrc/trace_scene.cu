@@ -14,9 +14,6 @@ namespace bhrt_b200 {
 #ifndef BHRT_SCENE_BLOCK
 #define BHRT_SCENE_BLOCK 128
 #endif
-#ifndef BHRT_SCENE_PERSISTENT
-#define BHRT_SCENE_PERSISTENT 0
-#endif
 constexpr int kBlock = BHRT_SCENE_BLOCK;
 constexpr int kSlots = 8;
 constexpr int kSphSm = 128;          // spheres staged in shared memory
@@ -509,12 +506,7 @@ __device__ __noinline__ Hit radial_scene(const KParams& p, V3 origin, V3 dir, do
 }
 
 template <int INTEG>
-#ifdef BHRT_SCENE_MAXNREG  // explicit register cap instead of a blocks-per-SM bound
-__global__ void __maxnreg__(BHRT_SCENE_MAXNREG)
-#else
-__global__ void __launch_bounds__(kBlock, BHRT_SCENE_MINB)
-#endif
-    trace_scene_kernel(const __grid_constant__ KParams p) {
+__global__ void __launch_bounds__(kBlock, BHRT_SCENE_MINB) trace_scene_kernel(const __grid_constant__ KParams p) {
     __shared__ SceneSm sm;
     const int t = threadIdx.x;
     // the fp32 prefilter is read only without the plane-angle cull table
@@ -527,21 +519,7 @@ __global__ void __launch_bounds__(kBlock, BHRT_SCENE_MINB)
     if (!p.cull) __syncthreads();  // uniform over the grid (kernel parameter)
 
     const long long n = (long long)p.n_rows * p.width * p.spp;
-#if BHRT_SCENE_PERSISTENT
-    // persistent blocks: each warp takes 32-sample tiles (8 pixels x 4 spp)
-    // from a global counter until the frame is done
-    unsigned long long tot_steps = 0, tot_rej = 0, tot_rays = 0;
-    const int lane = t & 31;
-    for (;;) {
-        unsigned tile = 0;
-        if (lane == 0) tile = atomicAdd(p.queue, 1u);
-        tile = __shfl_sync(0xffffffffu, tile, 0);
-        if ((long long)tile * 32 >= n) break;
-        const long long i = (long long)tile * 32 + lane;
-#else
-    {
-        const long long i = (long long)blockIdx.x * blockDim.x + t;
-#endif
+    const long long i = (long long)blockIdx.x * blockDim.x + t;
     unsigned nsteps = 0, nrej = 0;
     const bool valid = i < n;
     const SampleId id = sample_of(p, valid ? i : 0);
@@ -635,40 +613,12 @@ __global__ void __launch_bounds__(kBlock, BHRT_SCENE_MINB)
         }
     }
     finish_sample(p, valid, id, H.obj, H.sphere, H.point, phi, nsteps, nrej);
-#if BHRT_SCENE_PERSISTENT
-    tot_steps += nsteps;
-    tot_rej += nrej;
-    tot_rays += valid ? 1ull : 0ull;
-    }
-    warp_add_stats(p.stats, tot_steps, tot_rej, tot_rays);
-#else
     warp_add_stats(p.stats, nsteps, nrej, valid ? 1ull : 0ull);
-    }
-#endif
 }
 
 void launch_scene(const KParams& p, cudaStream_t st) {
     const long long n = (long long)p.n_rows * p.width * p.spp;
-#if BHRT_SCENE_PERSISTENT
-    static int per_sm[2][64] = {};  // resident blocks per SM by integrator and device
-    int dev = 0, sms = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int w = p.integrator == BHRT_INTEGRATOR_RK4 ? 0 : 1;
-    if (!per_sm[w][dev & 63]) {
-        if (w == 0)
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[w][dev & 63],
-                                                          trace_scene_kernel<BHRT_INTEGRATOR_RK4>, kBlock, 0);
-        else
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[w][dev & 63],
-                                                          trace_scene_kernel<BHRT_INTEGRATOR_RKF45>, kBlock, 0);
-        if (per_sm[w][dev & 63] < 1) per_sm[w][dev & 63] = 1;
-    }
-    const long long want = (n + kBlock - 1) / kBlock;
-    const unsigned blocks = (unsigned)(want < (long long)sms * per_sm[w][dev & 63] ? want : (long long)sms * per_sm[w][dev & 63]);
-#else
     const unsigned blocks = (unsigned)((n + kBlock - 1) / kBlock);
-#endif
     if (p.integrator == BHRT_INTEGRATOR_RK4)
         trace_scene_kernel<BHRT_INTEGRATOR_RK4><<<blocks, kBlock, 0, st>>>(p);
     else
