@@ -198,7 +198,6 @@ struct bhrt_ctx {
     DevBuf<double> checker;     // checker cell boundaries (KParams::checker_tab)
     DevBuf<uint8_t> out;
     DevBuf<unsigned long long> stats;
-    DevBuf<unsigned int> queue;
     DevBuf<unsigned long long> cull;
     DevBuf<double> tab_smp, tab_ends, tab_psi0;
     DevBuf<int32_t> tab_kind, tab_n;
@@ -363,7 +362,7 @@ int bhrt_ctx_create(int32_t device, bhrt_ctx** out, bhrt_status_info* info) {
     CK(cudaSetDevice(device));
     std::unique_ptr<bhrt_ctx> c(new bhrt_ctx());
     c->device = device;
-    if (c->stats.ensure(8) || c->queue.ensure(1) || c->tables.ensure(2 * kQN))
+    if (c->stats.ensure(8) || c->tables.ensure(2 * kQN))
         return set_info(info, BHRT_DEVICE, -1, -1, "bhrt_ctx_create: cudaMalloc failed");
     CK(cudaMallocHost(&c->host_stats, 16 * sizeof(unsigned long long)));
     CK(cudaStreamCreateWithFlags(&c->up_stream, cudaStreamNonBlocking));
@@ -413,7 +412,6 @@ void bhrt_ctx_destroy(bhrt_ctx* c) {
     c->records.release();
     c->out.release();
     c->stats.release();
-    c->queue.release();
     c->cull.release();
     c->checker.release();
     c->rays.release();
@@ -613,14 +611,12 @@ int bhrt_ctx_render_async(bhrt_ctx* c, int32_t row_start, int32_t row_end, int32
     k.out = d_out;
     k.out_image = c->out_image;
     k.stats = c->stats.p;
-    k.queue = c->queue.p;
     CK(cudaStreamWaitEvent(st, c->up_done, 0));  // the scene's uploads
     if (!c->in_frame) {  // counters + lowest failing pixel start fresh for this render
         CK(cudaMemcpyAsync(c->stats.p, c->host_stats + 8, 8 * sizeof(unsigned long long),
                            cudaMemcpyHostToDevice, st));
         c->launches = 0;
     }
-    CK(cudaMemsetAsync(c->queue.p, 0, sizeof(unsigned int), st));
     c->timed = c->timing && rows > 0;
     if (rows > 0 && launch_trace(k, st, &c->launches, c->timed ? c->ev : nullptr) != 0)
         return set_info(info, BHRT_INVALID_ARGUMENT, -1, -1, "render: unsupported integrator");

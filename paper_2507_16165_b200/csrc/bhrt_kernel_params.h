@@ -94,7 +94,6 @@ struct KParams {
     bhrt_ray_record* records;   // n_rows * width * spp
     uint8_t* out;               // n_rows * width * 3
     unsigned long long* stats;  // [0] steps, [1] rejected, [2] rays, [3] lowest failing y*width+x (ULLONG_MAX: none), [4..7] BHRT_COUNTERS
-    unsigned int* queue;        // persistent work counter
 };
 
 __host__ __device__ inline int packed_row_to_y(const KParams& p, int j) {
