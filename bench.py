@@ -139,17 +139,20 @@ def reference_sky_only(scene, rows: int, threads: int):
                       f"PPM), rows [{r0},{r1}) = {rays} rays, {dt:.1f} s"}
 
 
-def measure_secondary(device: int, reps: int = 3) -> dict:
+def measure_secondary(device: int, reps: int = 3, rank: int = 0, world: int = 1) -> dict:
     """Device-timed Mrays/s of configs 0, 1, 3 (scene resident, best of
-    `reps` after one warm-up) and config 4's whole 120-frame orbit on this GPU
-    (frames/s, wall clock, per-frame scene upload + cull table included)."""
+    `reps` after one warm-up) and config 4's whole 120-frame orbit (frames/s,
+    wall clock, per-frame scene upload + cull table included; with N ranks
+    the frames are sharded f mod N and the whole-box rate uses the slowest
+    rank). Everything but config 4 runs on rank 0 only."""
     import torch
+    import torch.distributed as dist
 
     from paper_2507_16165_b200 import render, scenes
     out = {}
     ctx = render.Context(device)
     st = torch.cuda.current_stream()
-    for idx in (0, 1, 3):
+    for idx in (0, 1, 3) if rank == 0 else ():
         sb = scenes.config(idx)
         t0 = time.perf_counter()
         ctx.set_scene(sb)
@@ -184,22 +187,33 @@ def measure_secondary(device: int, reps: int = 3) -> dict:
     ctx2 = render.Context(device)
     bufs = [buf, torch.empty_like(buf)]
     ctxs = [ctx, ctx2]
+    mine = scs[rank::world]  # frame sharding f mod N (BASELINE.json config 4)
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     t0 = time.perf_counter()
-    for f, sb in enumerate(scs):
+    for f, sb in enumerate(mine):
         c = ctxs[f % 2]
         c.set_scene(sb)
         c.render_async(bufs[f % 2].data_ptr(), stream=st.cuda_stream)
         if f > 0:
             ctxs[(f - 1) % 2].finish()
-    ctxs[(frames - 1) % 2].finish()
+    if mine:
+        ctxs[(len(mine) - 1) % 2].finish()
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
+    if world > 1:
+        tdt = torch.tensor([dt], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tdt, op=dist.ReduceOp.MAX)
+        dt = float(tdt.item())
     ctx2.close()
     out["config4"] = {"frames": frames, "seconds": dt, "frames/s": frames / dt,
                       "Mrays/s": frames * sb0.s.width * sb0.s.height * sb0.s.spp / dt / 1e6,
-                      "size": [sb0.s.width, sb0.s.height, sb0.s.spp],
-                      "note": "1 GPU; frames shard f mod N across GPUs"}
+                      "size": [sb0.s.width, sb0.s.height, sb0.s.spp], "n_gpus": world,
+                      "note": "frames sharded f mod N; whole-box rate = frames / slowest rank"}
+    if rank != 0:
+        ctx.close()
+        return out
     # strong-scaling projection on this one GPU: each rank's cyclic-row share
     # of the config-2 frame rendered alone (device time), max over ranks, vs
     # the whole frame / N. Communication is not included (the multi-GPU run
@@ -416,7 +430,7 @@ def run_ours(args):
     # ---- the other BASELINE.json configs (secondary lines, rank 0, this GPU)
     secondary = None
     if not args.no_secondary:
-        secondary = measure_secondary(local)
+        secondary = measure_secondary(local, rank=rank, world=world)
 
     # ---- CPU baseline on this box's host cores (rank 0, N=1 only)
     cpu = None
