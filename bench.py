@@ -421,9 +421,12 @@ def run_ours(args):
     achieved = (sum(flops) / len(flops)) / (avg_trace_ms * 1e-3) / 1e12
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
+    pipe_busy = None
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get(f"config{args.config}")
+            tj = json.load(open(tp))
+            traffic = tj.get(f"config{args.config}")
+            pipe_busy = tj.get(f"config{args.config}_fp64_pipe_active")
         except Exception:
             traffic = None
 
@@ -455,6 +458,7 @@ def run_ours(args):
                    "parallelism": f"cyclic rows x{world} + NCCL gather" if world > 1 else "1 GPU"},
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
+                     "fp64_pipe_active_ncu": pipe_busy,
                      "kernel": "trace_scene_kernel" if scene.s.integrator else "trace_reference_kernel",
                      "kernel_ms": avg_trace_ms, "shade_ms": sum(shade_ms) / len(shade_ms),
                      "peak_source": "K0 fp64 FMA microbenchmark measured in this run "
