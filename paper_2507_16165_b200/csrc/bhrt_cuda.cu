@@ -180,6 +180,15 @@ struct DevBuf {
     }
 };
 
+// Per-sample records for unfused shading (spp not dividing 32). Renders of one frame may run concurrently on several
+// streams, so each render takes a slot whose previous user has finished
+// (event), growing the pool up to kRecSlots; past that it waits on a slot.
+struct RecSlot {
+    DevBuf<bhrt_ray_record> buf;
+    cudaEvent_t done = nullptr;
+};
+constexpr size_t kRecSlots = 4;
+
 }  // namespace
 }  // namespace bhrt_b200
 
@@ -193,7 +202,9 @@ struct bhrt_ctx {
     DevBuf<uint8_t> sky;
     DevBuf<bhrt_sphere> spheres;
     DevBuf<double> tables;
-    DevBuf<bhrt_ray_record> records;
+    DevBuf<bhrt_ray_record> records;  // trace_rays / render_rows record outputs
+    std::vector<RecSlot*> rec_pool;   // unfused-shading scratch (RecSlot)
+    size_t rec_rr = 0;
     DevBuf<double> rays, defl;  // bhrt_cuda_trace_rays
     DevBuf<double> checker;     // checker cell boundaries (KParams::checker_tab)
     DevBuf<uint8_t> out;
@@ -410,6 +421,12 @@ void bhrt_ctx_destroy(bhrt_ctx* c) {
     c->spheres.release();
     c->tables.release();
     c->records.release();
+    for (RecSlot* r : c->rec_pool) {
+        r->buf.release();
+        if (r->done) cudaEventDestroy(r->done);
+        delete r;
+    }
+    c->rec_pool.clear();
     c->out.release();
     c->stats.release();
     c->cull.release();
@@ -603,9 +620,29 @@ int bhrt_ctx_render_async(bhrt_ctx* c, int32_t row_start, int32_t row_end, int32
     k.tile_offset = tile_offset;
     k.n_rows = rows;
     const size_t nrec = static_cast<size_t>(rows) * k.width * k.spp;
-    if (!d_records && !k.fused_shade) {  // unfused shading reads the records
-        if (c->records.ensure(nrec)) return set_info(info, BHRT_DEVICE, -1, -1, "records alloc failed");
-        d_records = c->records.p;
+    RecSlot* slot = nullptr;
+    if (!d_records && !k.fused_shade && rows > 0) {  // unfused shading reads the records
+        bool not_ready = false;
+        for (RecSlot* r : c->rec_pool) {
+            const cudaError_t q = cudaEventQuery(r->done);
+            if (q == cudaSuccess) {
+                slot = r;
+                break;
+            }
+            not_ready = not_ready || q == cudaErrorNotReady;
+        }
+        if (not_ready) (void)cudaGetLastError();  // "not ready" is a status, not an error
+        if (!slot && c->rec_pool.size() < kRecSlots) {
+            slot = new RecSlot;
+            c->rec_pool.push_back(slot);
+            CK(cudaEventCreateWithFlags(&slot->done, cudaEventDisableTiming));
+        }
+        if (!slot) {
+            slot = c->rec_pool[c->rec_rr++ % c->rec_pool.size()];
+            CK(cudaStreamWaitEvent(st, slot->done, 0));
+        }
+        if (slot->buf.ensure(nrec)) return set_info(info, BHRT_DEVICE, -1, -1, "records alloc failed");
+        d_records = slot->buf.p;
     }
     k.records = d_records;
     k.out = d_out;
@@ -621,6 +658,7 @@ int bhrt_ctx_render_async(bhrt_ctx* c, int32_t row_start, int32_t row_end, int32
     if (rows > 0 && launch_trace(k, st, &c->launches, c->timed ? c->ev : nullptr) != 0)
         return set_info(info, BHRT_INVALID_ARGUMENT, -1, -1, "render: unsupported integrator");
     CK(cudaGetLastError());
+    if (slot) CK(cudaEventRecord(slot->done, st));
     if (c->in_frame) {
         // counters accumulate on the device; finish() reads them once after
         // every render of the frame (its renders may run on several streams)

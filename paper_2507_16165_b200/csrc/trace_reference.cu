@@ -41,6 +41,23 @@ namespace bhrt_b200 {
 
 __device__ __forceinline__ double rhs_w(double u, double mass) { return 3.0 * mass * u * u - u; }
 
+// e / s of the error norm, bit-identical to the IEEE quotient. CUDA's double
+// division leaves its inline fast path for a subroutine when the quotient is
+// below ~2^-126 — including a zero numerator, which one of the two error
+// components is on ~45% of far-field steps. A zero numerator gives +-0
+// directly (s > 0); tiny ones are scaled by 2^900 first: a 2^900 is exact, its
+// quotient takes the fast path and (>= 2^-940, normal for |a| >= 2^-900,
+// s <= 2^40) scales back exactly, RN(a 2^900 / s) 2^-900 = RN(a / s)
+// (tools/div_scale_check.c).
+__device__ __forceinline__ double err_ratio(double e, double s) {
+    const double ae = fabs(e);
+    if (ae < 0x1p-120 && s > 0.0 && s <= 0x1p40) {
+        if (ae == 0.0) return e;
+        if (ae >= 0x1p-900) return ((e * 0x1p900) / s) * 0x1p-900;
+    }
+    return e / s;
+}
+
 // geodesic.cpp:84-162. Returns false on StepSizeUnderflow (phi/u/w then hold
 // the failure state, as StepSizeUnderflow::state does).
 // The step hint carried from one window to the next (geodesic.cpp:106,160):
@@ -130,8 +147,9 @@ __device__ bool integrate_window(double& phi, double& u, double& w, double dphi,
             // the divisions' and sqrt's denormal slow paths (frequent for
             // near-linear far-field windows). NaNs fail the test above.
         } else {
-            err += (e0 / s0) * (e0 / s0);
-            err += (e1 / s1) * (e1 / s1);
+            const double q0 = err_ratio(e0, s0), q1 = err_ratio(e1, s1);
+            err += q0 * q0;
+            err += q1 * q1;
             err = sqrt(err / 2.0);
         }
         if (err <= 1.0) {

@@ -133,7 +133,11 @@ __device__ BHRT_INL_SETUP double events_setup(const KParams& p, SceneSm& sm, int
         ++nc;
         return true;
     };
+#ifdef BHRT_EXPERIMENT_NOCAND
+    const int ns = 0;  // timing experiment only: no sphere candidates
+#else
     const int ns = p.n_spheres;
+#endif
     if (p.cull && ns > 0) {
         // plane-angle bin -> conservative sphere mask (host table, KParams::cull)
         const float na = (float)(n.x * p.cull_a[0] + n.y * p.cull_a[1] + n.z * p.cull_a[2]);
@@ -572,6 +576,10 @@ __global__ void __launch_bounds__(kBlock, BHRT_SCENE_MINB) trace_scene_kernel(co
                 }
             } else {
                 double h = p.step;
+#ifdef BHRT_EXPERIMENT_NOLOOP
+                H.obj = BHRT_OBJ_SKY;  // timing experiment only: setup + escape + shading
+                if (u < 0.0)
+#endif
                 for (;;) {  // geodesic.cpp:199-236 loop structure
                     if (u >= p.u_cap) { H.obj = BHRT_OBJ_HORIZON; break; }
                     if (u <= p.u_esc && w < 0.0) { H.obj = BHRT_OBJ_SKY; break; }

@@ -169,3 +169,15 @@ def test_render_rows_rejects_duplicate_devices_without_gpu():
     for devs in ([0, 0], [1, -1]):
         with pytest.raises(render.InvalidArgument, match="device"):
             render.render_rows(sb, 0, 1, devices=devs)
+
+
+def test_scaled_error_ratio_is_exact(tmp_path):
+    """err_ratio() (csrc/trace_reference.cu) divides tiny error terms with the
+    numerator scaled by 2^900; mode R's bit parity needs that to equal e / s."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = str(tmp_path / "div_scale_check")
+    subprocess.run(["gcc", "-O2", "-ffp-contract=off",
+                    os.path.join(root, "tools", "div_scale_check.c"), "-o", exe, "-lm"], check=True)
+    out = subprocess.run([exe, "10000000"], capture_output=True, text=True)
+    assert out.returncode == 0, out.stdout
+    assert out.stdout.startswith("0 mismatches")
