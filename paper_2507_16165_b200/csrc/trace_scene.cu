@@ -549,7 +549,7 @@ __global__ void __launch_bounds__(kBlock, BHRT_SCENE_MINB) trace_scene_kernel(co
             initial_conditions(p, dir, u, w);
             sm.energy[t] = w * w + u * u - (2.0 * p.mass) * u * u * u;
             double next_ev = events_setup(p, sm, t, B.e1, B.e2, nrm);
-            double pp = 0.0, up = 0.0, wp = 0.0;  // state before the last accepted step
+            double pp = 0.0, up = 0.0, wp = 0.0;  // RK4: state before the last accepted step
             bool has_step = false;
             if (INTEG == BHRT_INTEGRATOR_RK4) {
                 const double h = p.step;
@@ -580,44 +580,66 @@ __global__ void __launch_bounds__(kBlock, BHRT_SCENE_MINB) trace_scene_kernel(co
                 H.obj = BHRT_OBJ_SKY;  // timing experiment only: setup + escape + shading
                 if (u < 0.0)
 #endif
-                for (;;) {  // geodesic.cpp:199-236 loop structure
-                    if (u >= p.u_cap) { H.obj = BHRT_OBJ_HORIZON; break; }
-                    if (u <= p.u_esc && w < 0.0) { H.obj = BHRT_OBJ_SKY; break; }
-                    if (phi > p.phi_max) { H.obj = BHRT_OBJ_STALLED; break; }
-                    double un, wn, hn;
-                    // controller factors straight from the (L1-resident) global tables: measured
-                    // faster than staging them in shared memory (8.21 -> 8.05 ms, config 2)
-                    if (rkf45_step(u, w, h, p.M3, p.rel_tol, p.abs_tol, p.max_step, p.grow, p.shrink, un,
-                                   wn, hn)) {
-                        const double pn = phi + h;
-                        ++nsteps;
-                        if (pn >= next_ev && step_events(p, sm, t, phi, u, w, pn, un, wn, next_ev, H)) {
+                // geodesic.cpp:199-236 loop structure, with the capture and
+                // escape tests of the next trip evaluated right after the
+                // accepted step that produced the state (same tests, same
+                // order: numerical, capture, escape, then stall at the top):
+                // the escape direction then reads the step's end points from
+                // registers instead of a saved previous state.
+                if (u >= p.u_cap) {
+                    H.obj = BHRT_OBJ_HORIZON;
+                } else if (u <= p.u_esc && w < 0.0) {
+                    H.obj = BHRT_OBJ_SKY;
+                    H.point = escape_dir(p, sm, t, false, 0.0, 0.0, 0.0, phi, u, w);
+                } else {
+                    for (;;) {
+                        if (phi > p.phi_max) { H.obj = BHRT_OBJ_STALLED; break; }
+                        double un, wn, hn;
+                        // controller factors straight from the (L1-resident) global tables: measured
+                        // faster than staging them in shared memory (8.21 -> 8.05 ms, config 2)
+                        if (rkf45_step(u, w, h, p.M3, p.rel_tol, p.abs_tol, p.max_step, p.grow, p.shrink, un,
+                                       wn, hn)) {
+                            const double pn = phi + h;
+                            ++nsteps;
+                            if (pn >= next_ev && step_events(p, sm, t, phi, u, w, pn, un, wn, next_ev, H)) {
+                                phi = pn;
+                                break;
+                            }
+                            if (!(un > 0.0)) {
+                                H.obj = -BHRT_NUMERICAL;
+                                phi = pn;
+                                u = un;
+                                w = wn;
+                                break;
+                            }
+                            if (un >= p.u_cap) {
+                                H.obj = BHRT_OBJ_HORIZON;
+                                phi = pn;
+                                u = un;
+                                break;
+                            }
+                            if (un <= p.u_esc && wn < 0.0) {
+                                H.obj = BHRT_OBJ_SKY;
+                                H.point = escape_dir(p, sm, t, true, phi, u, w, pn, un, wn);
+                                phi = pn;
+                                break;
+                            }
                             phi = pn;
+                            u = un;
+                            w = wn;
+                        } else {
+                            ++nrej;
+                        }
+                        h = hn;
+                        if (h < 1e-14) {
+                            H.obj = (p.mass > 0.0 && u >= p.u_cap) ? BHRT_OBJ_HORIZON : -BHRT_NUMERICAL;
                             break;
                         }
-                        pp = phi;
-                        up = u;
-                        wp = w;
-                        has_step = true;
-                        phi = pn;
-                        u = un;
-                        w = wn;
-                        if (!(u > 0.0)) { H.obj = -BHRT_NUMERICAL; break; }
-                    } else {
-                        ++nrej;
-                    }
-                    h = hn;
-                    if (h < 1e-14) {
-                        H.obj = (p.mass > 0.0 && u >= p.u_cap) ? BHRT_OBJ_HORIZON : -BHRT_NUMERICAL;
-                        break;
                     }
                 }
             }
-#ifdef BHRT_EXPERIMENT_NOESCAPE
-            if (H.obj == BHRT_OBJ_SKY) H.point = mk(pp, up, wp);  // timing experiment only
-#else
-            if (H.obj == BHRT_OBJ_SKY) H.point = escape_dir(p, sm, t, has_step, pp, up, wp, phi, u, w);
-#endif
+            if (INTEG == BHRT_INTEGRATOR_RK4 && H.obj == BHRT_OBJ_SKY)
+                H.point = escape_dir(p, sm, t, has_step, pp, up, wp, phi, u, w);
         }
     }
     finish_sample(p, valid, id, H.obj, H.sphere, H.point, phi, nsteps, nrej);
