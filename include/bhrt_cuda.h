@@ -225,6 +225,20 @@ int bhrt_scene_format_text(const bhrt_scene* scene, char* buf, size_t cap, size_
 int bhrt_cuda_trace_rays(const bhrt_scene* scene, const double* rays, int64_t n, int32_t device,
                          bhrt_ray_record* records, double* deflection, bhrt_status_info* info);
 
+/* The same batch, also returning each ray's polyline: the reference's
+ * trace() RayPolyline::points (geodesic.hpp:62-65,107-108; geodesic.cpp:
+ * 164-238): the origin, then every epsilon-window end; radial rays and rays
+ * launched beyond the escape radius get the reference's two-point lines.
+ * Ray i's first min(npoints[i], max_points) points land at
+ * points + 3 * max_points * i (x, y, z doubles); npoints[i] is the full
+ * count, so npoints[i] > max_points means truncated — call again with
+ * max_points = max(npoints) (max_points = 0 only counts). Window ends are
+ * bit-identical to the reference's; the world points use the device cos/sin
+ * (within ulps of glibc's). Errors and records as bhrt_cuda_trace_rays. */
+int bhrt_cuda_trace_polylines(const bhrt_scene* scene, const double* rays, int64_t n, int32_t device,
+                              int32_t max_points, double* points, int32_t* npoints,
+                              bhrt_ray_record* records, bhrt_status_info* info);
+
 /* ---- persistent context: scene resident in HBM, async launches ---- */
 typedef struct bhrt_ctx bhrt_ctx;
 

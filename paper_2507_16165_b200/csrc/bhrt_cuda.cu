@@ -23,6 +23,8 @@ namespace bhrt_b200 {
 int launch_trace(const KParams& p, cudaStream_t st, int* launches, cudaEvent_t* ev);
 void launch_table_build(const KParams& p, double* smp, double* ends, int32_t* kind, int32_t* n, cudaStream_t st);
 void launch_table_bind(const KParams& p, double* ends, double* psi0, double u0, cudaStream_t st);
+void launch_trace_polylines(const KParams& p, const double* rays, long long n, bhrt_ray_record* records,
+                            double* pts, int cap, int* npoly, cudaStream_t st);
 void launch_trace_rays(const KParams& p, const double* rays, long long n, bhrt_ray_record* records,
                        double* defl, cudaStream_t st);
 
@@ -206,6 +208,8 @@ struct bhrt_ctx {
     std::vector<RecSlot*> rec_pool;   // unfused-shading scratch (RecSlot)
     size_t rec_rr = 0;
     DevBuf<double> rays, defl;  // bhrt_cuda_trace_rays
+    DevBuf<double> poly_pts;    // bhrt_cuda_trace_polylines
+    DevBuf<int32_t> poly_n;
     DevBuf<double> checker;     // checker cell boundaries (KParams::checker_tab)
     DevBuf<uint8_t> out;
     DevBuf<unsigned long long> stats;
@@ -433,6 +437,8 @@ void bhrt_ctx_destroy(bhrt_ctx* c) {
     c->checker.release();
     c->rays.release();
     c->defl.release();
+    c->poly_pts.release();
+    c->poly_n.release();
     if (c->host_stats) cudaFreeHost(c->host_stats);
     if (c->staging) cudaFreeHost(c->staging);
     if (c->up_done) cudaEventDestroy(c->up_done);
@@ -904,11 +910,8 @@ extern "C" int bhrt_cuda_render_rows(const bhrt_scene* s, int32_t row_start, int
 }
 
 // trace() / deflection_of_ray() for a batch of caller rays.
-extern "C" int bhrt_cuda_trace_rays(const bhrt_scene* s, const double* rays, int64_t n, int32_t device,
-                                    bhrt_ray_record* records, double* deflection,
-                                    bhrt_status_info* info) {
-    if (!s || n < 0 || (n > 0 && (!rays || !records)))
-        return set_info(info, BHRT_INVALID_ARGUMENT, -1, -1, "trace_rays: bad arguments");
+namespace {
+int trace_batch_prepare(const bhrt_scene* s, const double* rays, int64_t n, bhrt_status_info* info) {
     // trace(): validate(cfg) (geodesic.cpp:19-27) then the mass (:167)
     if (!(s->epsilon > 0.0))
         return set_info(info, BHRT_INVALID_ARGUMENT, -1, -1, "trace config: epsilon must be > 0");
@@ -929,17 +932,10 @@ extern "C" int bhrt_cuda_trace_rays(const bhrt_scene* s, const double* rays, int
             return set_info(info, BHRT_INVALID_ARGUMENT, static_cast<int>(i), -1,
                             "trace: ray origin is not outside the event horizon");
     }
-    if (n == 0) return 0;
-    std::lock_guard<std::mutex> lock(g_ctx_mu);
-    int dev = device;
-    if (dev < 0) CK(cudaGetDevice(&dev));
-    bhrt_ctx* c = nullptr;
-    int rc = cached_ctx(dev, &c, info);
-    if (rc) return rc;
-    CK(cudaSetDevice(dev));
-    if (c->rays.ensure(6 * static_cast<size_t>(n)) || c->records.ensure(static_cast<size_t>(n)) ||
-        (deflection && c->defl.ensure(static_cast<size_t>(n))))
-        return set_info(info, BHRT_DEVICE, -1, -1, "trace_rays: alloc failed");
+    return 0;
+}
+
+KParams trace_batch_params(const bhrt_scene* s) {
     KParams k;
     std::memset(&k, 0, sizeof k);
     k.mass = s->mass;
@@ -955,14 +951,73 @@ extern "C" int bhrt_cuda_trace_rays(const bhrt_scene* s, const double* rays, int
     k.rel_tol = s->rel_tol;
     k.abs_tol = s->abs_tol;
     k.ref_pow_prev0 = std::pow(1e-4, 0.4 / 5.0);  // host libm, as the reference
-    CK(cudaMemcpy(c->rays.p, rays, sizeof(double) * 6 * n, cudaMemcpyHostToDevice));
-    launch_trace_rays(k, c->rays.p, n, c->records.p, deflection ? c->defl.p : nullptr, nullptr);
-    CK(cudaGetLastError());
-    CK(cudaMemcpy(records, c->records.p, sizeof(bhrt_ray_record) * n, cudaMemcpyDeviceToHost));
-    if (deflection) CK(cudaMemcpy(deflection, c->defl.p, sizeof(double) * n, cudaMemcpyDeviceToHost));
+    return k;
+}
+
+int trace_batch_failures(const bhrt_ray_record* records, int64_t n, bhrt_status_info* info) {
     for (int64_t i = 0; i < n; ++i)
         if (records[i].object == -BHRT_NUMERICAL)
             return set_info(info, BHRT_NUMERICAL, static_cast<int>(i), -1,
                             "trace: inverse radius left the positive domain or step underflow");
     return 0;
+}
+}  // namespace
+
+extern "C" int bhrt_cuda_trace_rays(const bhrt_scene* s, const double* rays, int64_t n, int32_t device,
+                                    bhrt_ray_record* records, double* deflection,
+                                    bhrt_status_info* info) {
+    if (!s || n < 0 || (n > 0 && (!rays || !records)))
+        return set_info(info, BHRT_INVALID_ARGUMENT, -1, -1, "trace_rays: bad arguments");
+    int rc = trace_batch_prepare(s, rays, n, info);
+    if (rc) return rc;
+    if (n == 0) return 0;
+    std::lock_guard<std::mutex> lock(g_ctx_mu);
+    int dev = device;
+    if (dev < 0) CK(cudaGetDevice(&dev));
+    bhrt_ctx* c = nullptr;
+    rc = cached_ctx(dev, &c, info);
+    if (rc) return rc;
+    CK(cudaSetDevice(dev));
+    if (c->rays.ensure(6 * static_cast<size_t>(n)) || c->records.ensure(static_cast<size_t>(n)) ||
+        (deflection && c->defl.ensure(static_cast<size_t>(n))))
+        return set_info(info, BHRT_DEVICE, -1, -1, "trace_rays: alloc failed");
+    const KParams k = trace_batch_params(s);
+    CK(cudaMemcpy(c->rays.p, rays, sizeof(double) * 6 * n, cudaMemcpyHostToDevice));
+    launch_trace_rays(k, c->rays.p, n, c->records.p, deflection ? c->defl.p : nullptr, nullptr);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(records, c->records.p, sizeof(bhrt_ray_record) * n, cudaMemcpyDeviceToHost));
+    if (deflection) CK(cudaMemcpy(deflection, c->defl.p, sizeof(double) * n, cudaMemcpyDeviceToHost));
+    return trace_batch_failures(records, n, info);
+}
+
+// trace()'s RayPolyline for a batch of caller rays (geodesic.hpp:62-65,107-108).
+extern "C" int bhrt_cuda_trace_polylines(const bhrt_scene* s, const double* rays, int64_t n, int32_t device,
+                                         int32_t max_points, double* points, int32_t* npoints,
+                                         bhrt_ray_record* records, bhrt_status_info* info) {
+    if (!s || n < 0 || max_points < 0 || (n > 0 && (!rays || !records || !npoints)) ||
+        (n > 0 && max_points > 0 && !points))
+        return set_info(info, BHRT_INVALID_ARGUMENT, -1, -1, "trace_polylines: bad arguments");
+    int rc = trace_batch_prepare(s, rays, n, info);
+    if (rc) return rc;
+    if (n == 0) return 0;
+    const size_t npts = static_cast<size_t>(n) * static_cast<size_t>(max_points) * 3;
+    std::lock_guard<std::mutex> lock(g_ctx_mu);
+    int dev = device;
+    if (dev < 0) CK(cudaGetDevice(&dev));
+    bhrt_ctx* c = nullptr;
+    rc = cached_ctx(dev, &c, info);
+    if (rc) return rc;
+    CK(cudaSetDevice(dev));
+    if (c->rays.ensure(6 * static_cast<size_t>(n)) || c->records.ensure(static_cast<size_t>(n)) ||
+        c->poly_n.ensure(static_cast<size_t>(n)) || (npts > 0 && c->poly_pts.ensure(npts)))
+        return set_info(info, BHRT_DEVICE, -1, -1, "trace_polylines: alloc failed");
+    const KParams k = trace_batch_params(s);
+    CK(cudaMemcpy(c->rays.p, rays, sizeof(double) * 6 * n, cudaMemcpyHostToDevice));
+    launch_trace_polylines(k, c->rays.p, n, c->records.p, npts > 0 ? c->poly_pts.p : nullptr, max_points,
+                           c->poly_n.p, nullptr);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(records, c->records.p, sizeof(bhrt_ray_record) * n, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(npoints, c->poly_n.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost));
+    if (npts > 0) CK(cudaMemcpy(points, c->poly_pts.p, sizeof(double) * npts, cudaMemcpyDeviceToHost));
+    return trace_batch_failures(records, n, info);
 }

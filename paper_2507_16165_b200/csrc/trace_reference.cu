@@ -191,6 +191,14 @@ __device__ __forceinline__ V3 plane_point(V3 origin, V3 e1, V3 e2, double r, dou
     return add(origin, scl(add(scl(e1, cos(phi)), scl(e2, sin(phi))), r));
 }
 
+__device__ __forceinline__ void poly_put(double* pts, int cap, int k, V3 q) {
+    if (k < cap) {
+        pts[3 * k] = q.x;
+        pts[3 * k + 1] = q.y;
+        pts[3 * k + 2] = q.z;
+    }
+}
+
 struct RResult {
     int obj;        // HORIZON / SKY / STALLED or -BHRT_NUMERICAL
     V3 edir;        // escape direction (SKY with at least one window)
@@ -204,9 +212,14 @@ struct RResult {
 // last two window ends are kept; the escape direction is the normalised last
 // chord of the polyline (geodesic.cpp:211-212). With DEFL the per-segment
 // turning of deflection_of_ray (geodesic.cpp:248-260) is accumulated too.
-template <bool DEFL>
+// With POLY the polyline itself is written too (trace()'s RayPolyline::points,
+// geodesic.cpp:195-236): pts[k] for k < cap (3 doubles each), the full point
+// count in npoly (which may exceed cap: the caller re-runs with more room).
+template <bool DEFL, bool POLY = false>
 __device__ __forceinline__ RResult window_loop(const KParams& p, V3 origin, V3 center, V3 e1, V3 e2,
-                                               double u, double w, unsigned& nsteps, unsigned& nrej) {
+                                               double u, double w, unsigned& nsteps, unsigned& nrej,
+                                               double* pts = nullptr, int cap = 0, int* npoly = nullptr,
+                                               V3 ray_dir = {0.0, 0.0, 0.0}) {
     RResult R;
     R.obj = BHRT_OBJ_NONE;
     R.edir = mk(0.0, 0.0, 0.0);
@@ -218,11 +231,15 @@ __device__ __forceinline__ RResult window_loop(const KParams& p, V3 origin, V3 c
     int npts = 1;
     V3 p_prev = origin;
     double prev_x = 0.0, prev_y = 0.0;
+    if (POLY) poly_put(pts, cap, 0, origin);
     for (;;) {
         if (u >= p.u_cap) { R.obj = BHRT_OBJ_HORIZON; break; }
         if (u <= p.u_esc && w < 0.0) {
             R.obj = BHRT_OBJ_SKY;
-            if (npts >= 2) {
+            const bool had_window = npts >= 2;
+            if (POLY && !had_window)  // launched beyond the escape radius moving outward
+                poly_put(pts, cap, npts++, add(origin, scl(ray_dir, p.escape_radius)));
+            if (had_window) {
                 const V3 last = plane_point(center, e1, e2, 1.0 / last_u, last_phi);
                 const V3 prev = npts == 2 ? origin : plane_point(center, e1, e2, 1.0 / prev_u, prev_phi);
                 R.edir = normalized(sub(last, prev));
@@ -236,7 +253,15 @@ __device__ __forceinline__ RResult window_loop(const KParams& p, V3 origin, V3 c
         const double dphi = clampd(p.epsilon * u * u / hyp, 1e-6, 0.1);
         if (!integrate_window(phi, u, w, dphi, p.mass, p.rel_tol, p.abs_tol, hs, nsteps, nrej,
                               p.ref_pow_prev0)) {
-            if (p.mass > 0.0 && u >= p.u_cap) { R.obj = BHRT_OBJ_HORIZON; break; }
+            if (p.mass > 0.0 && u >= p.u_cap) {
+                if (POLY) {  // the underflow point, unless it repeats the last one (geodesic.cpp:222-224)
+                    const V3 q = plane_point(center, e1, e2, 1.0 / u, phi);
+                    const V3 last = npts == 1 ? origin : plane_point(center, e1, e2, 1.0 / last_u, last_phi);
+                    if (norm(sub(q, last)) > 0.0) poly_put(pts, cap, npts++, q);
+                }
+                R.obj = BHRT_OBJ_HORIZON;
+                break;
+            }
             R.obj = -BHRT_NUMERICAL;
             break;
         }
@@ -245,6 +270,7 @@ __device__ __forceinline__ RResult window_loop(const KParams& p, V3 origin, V3 c
         prev_u = last_u;
         last_phi = phi;
         last_u = u;
+        if (POLY) poly_put(pts, cap, npts, plane_point(center, e1, e2, 1.0 / u, phi));
         ++npts;
         if (DEFL) {
             const V3 pt = plane_point(center, e1, e2, 1.0 / u, phi);
@@ -257,6 +283,7 @@ __device__ __forceinline__ RResult window_loop(const KParams& p, V3 origin, V3 c
         }
     }
     R.phi = phi;
+    if (POLY) *npoly = npts;
     return R;
 }
 
@@ -299,9 +326,12 @@ __global__ void __launch_bounds__(128, BHRT_REF_MINB) trace_reference_kernel(con
 // initial state follow geodesic.cpp:49-65 (oracle orc_plane_basis /
 // orc_initial_conditions, same operations). Origins inside the horizon are
 // rejected on the host before launch.
-template <bool DEFL>
+// With POLY (bhrt_cuda_trace_polylines) each ray also writes its polyline:
+// up to cap points at pts + 3 cap i, the full count at npoly[i].
+template <bool DEFL, bool POLY>
 __global__ void __launch_bounds__(128, BHRT_REF_MINB) trace_rays_kernel(const __grid_constant__ KParams p, const double* rays,
-                                                         long long n, bhrt_ray_record* records, double* defl) {
+                                                         long long n, bhrt_ray_record* records, double* defl,
+                                                         double* pts, int cap, int* npoly) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const V3 origin = vld(rays + 6 * i), dir = vld(rays + 6 * i + 3), center = vld(p.center);
@@ -317,12 +347,21 @@ __global__ void __launch_bounds__(128, BHRT_REF_MINB) trace_rays_kernel(const __
     if (norm(tangential) < 1e-12) {  // radial: geodesic.cpp:175-187
         rec.object = dot(dir, sub(center, origin)) > 0.0 ? BHRT_OBJ_HORIZON : BHRT_OBJ_SKY;
         if (rec.object == BHRT_OBJ_SKY) pt = dir;
+        if (POLY) {
+            double* q = pts + (size_t)3 * cap * i;
+            poly_put(q, cap, 0, origin);
+            const double len = rec.object == BHRT_OBJ_SKY ? p.escape_radius : norm(v) - 2.0 * p.mass;
+            poly_put(q, cap, 1, add(origin, scl(dir, len)));
+            npoly[i] = 2;
+        }
     } else {
         const V3 e2 = normalized(tangential);
         const double r0 = norm(v);
         const double b = norm(cross(v, dir));
         const double u = 1.0 / r0, w = -dot(v, dir) / (r0 * b);
-        const RResult R = window_loop<DEFL>(p, origin, center, e1, e2, u, w, nsteps, nrej);
+        const RResult R = window_loop<DEFL, POLY>(p, origin, center, e1, e2, u, w, nsteps, nrej,
+                                                  POLY ? pts + (size_t)3 * cap * i : nullptr, cap,
+                                                  POLY ? npoly + i : nullptr, dir);
         rec.object = R.obj;
         if (R.obj == BHRT_OBJ_SKY) pt = R.chord ? R.edir : dir;
         rec.phi = R.phi;
@@ -341,9 +380,15 @@ void launch_trace_rays(const KParams& p, const double* rays, long long n, bhrt_r
                        double* defl, cudaStream_t st) {
     const unsigned blocks = (unsigned)((n + 127) / 128);
     if (defl)
-        trace_rays_kernel<true><<<blocks, 128, 0, st>>>(p, rays, n, records, defl);
+        trace_rays_kernel<true, false><<<blocks, 128, 0, st>>>(p, rays, n, records, defl, nullptr, 0, nullptr);
     else
-        trace_rays_kernel<false><<<blocks, 128, 0, st>>>(p, rays, n, records, nullptr);
+        trace_rays_kernel<false, false><<<blocks, 128, 0, st>>>(p, rays, n, records, nullptr, nullptr, 0, nullptr);
+}
+
+void launch_trace_polylines(const KParams& p, const double* rays, long long n, bhrt_ray_record* records,
+                            double* pts, int cap, int* npoly, cudaStream_t st) {
+    const unsigned blocks = (unsigned)((n + 127) / 128);
+    trace_rays_kernel<false, true><<<blocks, 128, 0, st>>>(p, rays, n, records, nullptr, pts, cap, npoly);
 }
 
 #ifdef BHRT_HINT_COUNT

@@ -4,16 +4,19 @@ batch entry point `bhrt_cuda_trace_rays`:
 
     BlackHole, TraceConfig                     geodesic.hpp:14-45
     TraceOutcome                               geodesic.hpp:51-60
-    trace(origin, dir, hole, cfg)              geodesic.hpp:107-108  (outcome, no polyline)
+    RayPolyline                                geodesic.hpp:62-65
+    trace(origin, dir, hole, cfg)              geodesic.hpp:107-108  (outcome; polyline=True: RayPolyline)
     deflection_of_ray(origin, dir, hole, cfg)  geodesic.hpp:110-113
     deflection_angle(b, hole, cfg)             geodesic.hpp:115-118
     trace_batch(origins, dirs, hole, cfg, deflection=False)   many rays, one launch
+    trace_polylines(origins, dirs, hole, cfg)  many rays with their polylines
 
 Errors follow the reference: invalid configuration or an origin inside the
 horizon -> InvalidArgument (std::invalid_argument), numerical failure or a
-deflection of a non-escaping ray -> NumericalError. The polyline itself is
-never materialised on the GPU; outcomes carry the escape direction (the
-normalised last chord, geodesic.cpp:211-212), step counts and the final phi.
+deflection of a non-escaping ray -> NumericalError. Outcomes carry the
+escape direction (the normalised last chord, geodesic.cpp:211-212), step
+counts and the final phi; the polyline is written only when asked for
+(bhrt_cuda_trace_polylines: a counting pass, then the points).
 """
 from __future__ import annotations
 
@@ -101,16 +104,72 @@ def trace_batch(origins, dirs, hole: BlackHole = BlackHole(), cfg: TraceConfig =
     return rec, defl
 
 
-def trace(ray_origin, ray_dir, hole: BlackHole = BlackHole(),
-          cfg: TraceConfig = TraceConfig()) -> TraceOutcome:
-    """geodesic.hpp:107-108 for one ray (outcome only)."""
-    rec, _ = trace_batch([ray_origin], [ray_dir], hole, cfg)
-    r = rec[0]
-    if r["object"] < 0:
-        raise NumericalError(BHRT_NUMERICAL, 0, -1, "trace: numerical failure")
+@dataclass
+class RayPolyline:  # geodesic.hpp:62-65
+    points: np.ndarray  # (k, 3) world points: the origin, then every window end
+    outcome: TraceOutcome
+
+
+def _outcome(r) -> TraceOutcome:
     kind = _KIND[int(r["object"])]
     edir = tuple(float(x) for x in r["point"]) if kind == "escaped" else (0.0, 0.0, 0.0)
     return TraceOutcome(kind, edir, int(r["steps"]), int(r["rejected"]), float(r["phi"]))
+
+
+def trace_polylines(origins, dirs, hole: BlackHole = BlackHole(), cfg: TraceConfig = TraceConfig(),
+                    device: int = -1, max_points: int | None = None):
+    """Traces n rays and returns (records, [points (k_i, 3) arrays]). With
+    max_points=None a counting pass sizes the buffer first; otherwise longer
+    polylines raise InvalidArgument (truncated). Errors as trace_batch."""
+    o = np.ascontiguousarray(np.asarray(origins, np.float64).reshape(-1, 3))
+    d = np.ascontiguousarray(np.asarray(dirs, np.float64).reshape(-1, 3))
+    if o.shape != d.shape:
+        raise InvalidArgument(BHRT_INVALID_ARGUMENT, -1, -1, "trace_polylines: origins/dirs shape mismatch")
+    n = o.shape[0]
+    rays = np.ascontiguousarray(np.concatenate([o, d], axis=1))
+    sb = _scene(hole, cfg)
+    L = native.lib()
+
+    def run(cap):
+        rec = np.zeros(n, record_dtype())
+        cnt = np.zeros(n, np.int32)
+        pts = np.zeros((n, max(cap, 0), 3))
+        info = StatusInfo()
+        rc = L.bhrt_cuda_trace_polylines(
+            sb.ptr(), rays.ctypes.data_as(C.POINTER(C.c_double)), n, device, cap,
+            pts.ctypes.data_as(C.POINTER(C.c_double)) if cap > 0 else None,
+            cnt.ctypes.data_as(C.POINTER(C.c_int32)), rec.ctypes.data_as(C.POINTER(RayRecord)),
+            C.byref(info))
+        if rc == BHRT_INVALID_ARGUMENT:
+            raise InvalidArgument(rc, info.px, info.py, info.message.decode(errors="replace"))
+        if rc not in (0, BHRT_NUMERICAL):
+            raise native.BhrtError(rc, info.px, info.py, info.message.decode(errors="replace"))
+        return rec, cnt, pts
+
+    cap = max_points
+    if cap is None:
+        _, cnt, _ = run(0)
+        cap = int(cnt.max()) if n else 0
+    rec, cnt, pts = run(cap)
+    if n and int(cnt.max()) > cap:
+        raise InvalidArgument(BHRT_INVALID_ARGUMENT, int(np.argmax(cnt)), -1,
+                              "trace_polylines: polyline longer than max_points")
+    return rec, [pts[i, :cnt[i]].copy() for i in range(n)]
+
+
+def trace(ray_origin, ray_dir, hole: BlackHole = BlackHole(),
+          cfg: TraceConfig = TraceConfig(), polyline: bool = False):
+    """geodesic.hpp:107-108 for one ray: the TraceOutcome, or with
+    polyline=True the reference's RayPolyline (points + outcome)."""
+    if polyline:
+        rec, pts = trace_polylines([ray_origin], [ray_dir], hole, cfg)
+    else:
+        rec, _ = trace_batch([ray_origin], [ray_dir], hole, cfg)
+    r = rec[0]
+    if r["object"] < 0:
+        raise NumericalError(BHRT_NUMERICAL, 0, -1, "trace: numerical failure")
+    out = _outcome(r)
+    return RayPolyline(pts[0], out) if polyline else out
 
 
 def deflection_of_ray(ray_origin, ray_dir, hole: BlackHole = BlackHole(),

@@ -47,6 +47,9 @@ def lib():
                                             P(StatusInfo)]
         L.bhrt_cuda_trace_rays.argtypes = [P(Scene), P(C.c_double), C.c_int64, C.c_int32,
                                            P(RayRecord), P(C.c_double), P(StatusInfo)]
+        L.bhrt_cuda_trace_polylines.argtypes = [P(Scene), P(C.c_double), C.c_int64, C.c_int32,
+                                                C.c_int32, P(C.c_double), P(C.c_int32),
+                                                P(RayRecord), P(StatusInfo)]
         L.bhrt_scene_parse_text.argtypes = [C.c_char_p, P(Scene), P(Sphere), C.c_int32,
                                             P(C.c_int32), P(StatusInfo)]
         L.bhrt_scene_format_text.argtypes = [P(Scene), C.c_char_p, C.c_size_t, P(C.c_size_t)]
@@ -83,7 +86,7 @@ def lib():
 # Symbols include/bhrt_cuda.h declares (checked by tests/test_abi.py).
 EXPORTS = [
     "bhrt_scene_defaults", "bhrt_validate_scene", "bhrt_make_spheres", "bhrt_make_bands",
-    "bhrt_cuda_render_rows", "bhrt_cuda_trace_rays", "bhrt_scene_parse_text",
+    "bhrt_cuda_render_rows", "bhrt_cuda_trace_rays", "bhrt_cuda_trace_polylines", "bhrt_scene_parse_text",
     "bhrt_scene_format_text", "bhrt_ctx_set_output_layout", "bhrt_device_alloc",
     "bhrt_device_free", "bhrt_ipc_export", "bhrt_ipc_open", "bhrt_ipc_close", "bhrt_ctx_create", "bhrt_ctx_destroy", "bhrt_ctx_set_scene",
     "bhrt_ctx_render_async", "bhrt_ctx_frame_begin", "bhrt_ctx_finish", "bhrt_ctx_stats", "bhrt_ctx_set_timing",

@@ -161,6 +161,16 @@ def test_trace_rays_host_validation_without_gpu():
     assert len(rec) == 0 and len(defl) == 0
     with pytest.raises(G.InvalidArgument, match="deflection_angle"):
         G.deflection_angle(0.0)
+    # the polyline entry point validates the same way, plus its own arguments
+    with pytest.raises(G.InvalidArgument, match="epsilon"):
+        G.trace_polylines([(20, 0, 0)], [(0, 1, 0)], G.BlackHole(1.0), G.TraceConfig(epsilon=0.0))
+    with pytest.raises(G.InvalidArgument, match="horizon") as e:
+        G.trace_polylines([(20, 0, 0), (1, 0, 0)], [(0, 1, 0)] * 2, G.BlackHole(1.0), c)
+    assert e.value.px == 1
+    with pytest.raises(G.InvalidArgument, match="bad arguments"):
+        G.trace_polylines([(20, 0, 0)], [(0, 1, 0)], G.BlackHole(1.0), c, max_points=-1)
+    rec, pts = G.trace_polylines(np.zeros((0, 3)), np.zeros((0, 3)), G.BlackHole(1.0), c)
+    assert len(rec) == 0 and pts == []
 
 
 def test_render_rows_rejects_duplicate_devices_without_gpu():
