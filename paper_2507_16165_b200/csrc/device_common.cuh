@@ -149,17 +149,31 @@ __device__ __forceinline__ void initial_conditions(const KParams& p, V3 dir, dou
 }
 
 // ----------------------------------------------------------------- record / stats helpers
-__device__ __forceinline__ void warp_add_stats(unsigned long long* stats, unsigned long long steps,
-                                               unsigned long long rej, unsigned long long rays) {
-    for (int o = 16; o > 0; o >>= 1) {
-        steps += __shfl_down_sync(0xffffffffu, steps, o);
-        rej += __shfl_down_sync(0xffffffffu, rej, o);
-        rays += __shfl_down_sync(0xffffffffu, rays, o);
+// Per-warp counter totals, one 64-bit atomic per counter from lane 0. The
+// per-lane counts are 32-bit; while every lane's count is below 2^26 the
+// warp sum fits 32 bits and one REDUX (__reduce_add_sync) forms it,
+// otherwise the 64-bit shuffle tree does.
+__device__ __forceinline__ void warp_add_stats(unsigned long long* stats, unsigned steps, unsigned rej,
+                                               unsigned rays) {
+    unsigned long long s, r, n;
+    if (__all_sync(0xffffffffu, steps < (1u << 26) && rej < (1u << 26))) {
+        s = __reduce_add_sync(0xffffffffu, steps);
+        r = __reduce_add_sync(0xffffffffu, rej);
+        n = __reduce_add_sync(0xffffffffu, rays);
+    } else {
+        s = steps;
+        r = rej;
+        n = rays;
+        for (int o = 16; o > 0; o >>= 1) {
+            s += __shfl_down_sync(0xffffffffu, s, o);
+            r += __shfl_down_sync(0xffffffffu, r, o);
+            n += __shfl_down_sync(0xffffffffu, n, o);
+        }
     }
     if ((threadIdx.x & 31) == 0) {
-        atomicAdd(&stats[0], steps);
-        atomicAdd(&stats[1], rej);
-        atomicAdd(&stats[2], rays);
+        atomicAdd(&stats[0], s);
+        atomicAdd(&stats[1], r);
+        atomicAdd(&stats[2], n);
     }
 }
 

@@ -375,7 +375,7 @@ __global__ void __launch_bounds__(128, BHRT_TAB_MINB) trace_table_kernel(const _
         }
     }
     finish_sample(p, valid, id, obj, -1, point, phi_out, 0u, 0u);
-    warp_add_stats(p.stats, 0ull, 0ull, valid ? 1ull : 0ull);
+    warp_add_stats(p.stats, 0u, 0u, valid ? 1u : 0u);
 }
 
 void launch_table_build(const KParams& p, double* smp, double* ends, int32_t* kind, int32_t* n, cudaStream_t st) {

@@ -316,7 +316,7 @@ __global__ void __launch_bounds__(128, BHRT_REF_MINB) trace_reference_kernel(con
         }
     }
     finish_sample(p, valid, id, obj, -1, edir, phi_end, nsteps, nrej);
-    warp_add_stats(p.stats, nsteps, nrej, valid ? 1ull : 0ull);
+    warp_add_stats(p.stats, nsteps, nrej, valid ? 1u : 0u);
 }
 
 // Ray batch (bhrt_cuda_trace_rays): the reference's

@@ -643,7 +643,7 @@ __global__ void __launch_bounds__(kBlock, BHRT_SCENE_MINB) trace_scene_kernel(co
         }
     }
     finish_sample(p, valid, id, H.obj, H.sphere, H.point, phi, nsteps, nrej);
-    warp_add_stats(p.stats, nsteps, nrej, valid ? 1ull : 0ull);
+    warp_add_stats(p.stats, nsteps, nrej, valid ? 1u : 0u);
 }
 
 void launch_scene(const KParams& p, cudaStream_t st) {
