@@ -68,8 +68,8 @@ __device__ __forceinline__ double err_ratio(double e, double s) {
 __device__ unsigned long long g_hint_count[4];  // developer counters: exact hints, binding hints, multi-step windows
 #endif
 struct HintState {
-    double h_try, err, pprev;  // last accepted step, its error norm, err_prev^0.08
-    bool pending;              // false: no hint yet (hint = 0 in the reference)
+    double h_try, err2, pprev;  // last accepted step, its squared error norm (see below), err_prev^0.08
+    bool pending;               // false: no hint yet (hint = 0 in the reference)
 };
 
 // First step size of a window: min(hint, dphi), or dphi without a hint.
@@ -78,18 +78,17 @@ struct HintState {
 // the device pow is skipped; otherwise the exact double is formed.
 __device__ __forceinline__ double window_h0(const HintState& hs, double dphi) {
     if (!hs.pending) return dphi;
-    const float ef = (float)hs.err;
-    if (hs.err >= 0.0 && ef <= 1.0f) {
-        // err <= 1e-30: err^-0.14 >= 1.58e4, pprev >= 1e-4^0.08 = 0.48, so the
+    if (hs.err2 >= 0.0 && hs.err2 <= 1.0 + 0x1p-52) {
+        // err^2 <= 1e-30: err^-0.14 >= 126, pprev >= 1e-4^0.08 = 0.48, so the
         // factor is clamped to exactly 5 (also for err = 0: pow -> inf)
         float lo = 5.0f;
-        if (ef > 1e-30f) {
-            const float lf = 0.9f * exp2f(-0.14f * __log2f(ef)) * (float)hs.pprev;
+        if (hs.err2 > 1e-30) {  // err^-0.14 = (err^2)^-0.07
+            const float lf = 0.9f * exp2f(-0.07f * __log2f((float)hs.err2)) * (float)hs.pprev;
             lo = fminf(fmaxf(lf * 0.999f, 0.2f), 5.0f);
         }
         if ((float)hs.h_try * lo >= (float)dphi * 1.00001f) return dphi;
     }
-    const double factor = clampd(0.9 * pow(hs.err, -0.7 / 5.0) * hs.pprev, 0.2, 5.0);
+    const double factor = clampd(0.9 * pow(sqrt(hs.err2), -0.7 / 5.0) * hs.pprev, 0.2, 5.0);
     const double hint = hs.h_try * factor;
 #ifdef BHRT_HINT_COUNT
     atomicAdd(&g_hint_count[0], 1ull);
@@ -137,7 +136,11 @@ __device__ bool integrate_window(double& phi, double& u, double& w, double dphi,
         const double e1 = h_try * (E1 * k11 + E3 * k31 + E4 * k41 + E5 * k51 + E6 * k61 + E7 * k71);
         const double s0 = atol + rtol * dmax(fabs(y0), fabs(n0));
         const double s1 = atol + rtol * dmax(fabs(y1), fabs(n1));
-        double err = 0.0;
+        // err2 = the reference's err before its sqrt (geodesic.cpp:125-130);
+        // err = sqrt(err2) is formed only where a pow needs it (rare). The
+        // acceptance test err <= 1 is err2 <= 1 + 2^-52: RN(sqrt(x)) <= 1 iff
+        // sqrt(x) <= 1 + 2^-53 (ties to even), i.e. x <= 1 + 2^-52 + 2^-106.
+        double err2 = 0.0;
         const double tiny = 1e-42 * atol;
         if (fabs(e0) < tiny && fabs(e1) < tiny) {
             // s >= atol, so the norm is < 1e-42 < 1e-30. Every later use of
@@ -148,11 +151,11 @@ __device__ bool integrate_window(double& phi, double& u, double& w, double dphi,
             // near-linear far-field windows). NaNs fail the test above.
         } else {
             const double q0 = err_ratio(e0, s0), q1 = err_ratio(e1, s1);
-            err += q0 * q0;
-            err += q1 * q1;
-            err = sqrt(err / 2.0);
+            err2 += q0 * q0;
+            err2 += q1 * q1;
+            err2 = err2 / 2.0;
         }
-        if (err <= 1.0) {
+        if (err2 <= 1.0 + 0x1p-52) {
             y0 = n0;
             y1 = n1;
             k10 = k70;
@@ -160,9 +163,10 @@ __device__ bool integrate_window(double& phi, double& u, double& w, double dphi,
             remaining -= h_try;
             ++nsteps;
             if (!(remaining > 0.0)) {  // window done: the hint is formed lazily (window_h0)
-                hs = {h_try, err, pprev, true};
+                hs = {h_try, err2, pprev, true};
                 break;
             }
+            const double err = sqrt(err2);
 #ifdef BHRT_HINT_COUNT
             atomicAdd(&g_hint_count[2], 1ull);
 #endif
@@ -170,7 +174,7 @@ __device__ bool integrate_window(double& phi, double& u, double& w, double dphi,
             err_prev = dmax(err, 1e-4);
             pprev = pow(err_prev, 0.4 / 5.0);
         } else {
-            h = h_try * clampd(0.9 * pow(err, -0.2), 0.1, 0.9);
+            h = h_try * clampd(0.9 * pow(sqrt(err2), -0.2), 0.1, 0.9);
             ++nrej;
         }
         if (h < 1e-14 && remaining > 0.0) {

@@ -191,3 +191,18 @@ def test_scaled_error_ratio_is_exact(tmp_path):
     out = subprocess.run([exe, "10000000"], capture_output=True, text=True)
     assert out.returncode == 0, out.stdout
     assert out.stdout.startswith("0 mismatches")
+
+
+def test_sqrt_acceptance_threshold():
+    """integrate_window (csrc/trace_reference.cu) tests err2 <= 1 + 2^-52
+    instead of sqrt(err2) <= 1: equal for every double near 1 (IEEE sqrt)."""
+    x = np.float64(1.0)
+    xs = [x]
+    lo = hi = x
+    for _ in range(64):
+        lo = np.nextafter(lo, 0.0)
+        hi = np.nextafter(hi, 2.0)
+        xs += [lo, hi]
+    xs = np.array(xs + [0.0, 1e-300, 0.5, 2.0, np.inf, np.nan])
+    with np.errstate(invalid="ignore"):
+        assert np.array_equal(np.sqrt(xs) <= 1.0, xs <= 1.0 + 2.0 ** -52)
