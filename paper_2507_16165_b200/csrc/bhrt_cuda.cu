@@ -490,6 +490,8 @@ int bhrt_ctx_set_scene(bhrt_ctx* c, const bhrt_scene* s, bhrt_status_info* info)
     k.tan_half_y = std::tan(s->vertical_fov / 2.0);  // camera.cpp:46-48
     const double aspect = static_cast<double>(s->width) / s->height;
     k.tan_half_x = k.tan_half_y * aspect;
+    k.inv_width = 1.0 / s->width;  // camera_ray: (px + sx) / width by reciprocal + fma correction
+    k.inv_height = 1.0 / s->height;
     k.width = s->width;
     k.height = s->height;
     k.spp = s->spp;

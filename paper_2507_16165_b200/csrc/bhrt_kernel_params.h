@@ -31,6 +31,7 @@ struct KParams {
     double cam_pos[3];
     double forward[3], right[3], up[3];
     double tan_half_x, tan_half_y;
+    double inv_width, inv_height;  // RN(1/width), RN(1/height)
     int32_t width, height, spp;
     int32_t pad0;
     uint64_t seed;

@@ -74,8 +74,15 @@ __device__ __forceinline__ V3 camera_ray(const KParams& p, int px, int py, int s
         sx = to_unit(hash_counter(p.seed, (uint64_t)px, (uint64_t)py, 2 * (uint64_t)sample));
         sy = to_unit(hash_counter(p.seed, (uint64_t)px, (uint64_t)py, 2 * (uint64_t)sample + 1));
     }
-    const double u = (px + sx) / p.width;
-    const double v = (py + sy) / p.height;
+    // (px + sx) / width as RN(a y) plus one Markstein correction with the
+    // host's y = RN(1/width): the correctly rounded quotient for these
+    // operands (a in [0, 2^16), width < 2^16: no under/overflow), i.e. the
+    // same double as the division (tools/div_check.c checks every width < 2^16;
+    // tests/test_abi.py::test_camera_division_is_exact).
+    const double au = px + sx, av = py + sy;
+    const double qu = au * p.inv_width, qv = av * p.inv_height;
+    const double u = fma(fma(-qu, (double)p.width, au), p.inv_width, qu);
+    const double v = fma(fma(-qv, (double)p.height, av), p.inv_height, qv);
     const V3 d = add(add(vld(p.forward), scl(vld(p.right), (2.0 * u - 1.0) * p.tan_half_x)),
                      scl(vld(p.up), (1.0 - 2.0 * v) * p.tan_half_y));
     return normalized(d);

@@ -206,3 +206,16 @@ def test_sqrt_acceptance_threshold():
     xs = np.array(xs + [0.0, 1e-300, 0.5, 2.0, np.inf, np.nan])
     with np.errstate(invalid="ignore"):
         assert np.array_equal(np.sqrt(xs) <= 1.0, xs <= 1.0 + 2.0 ** -52)
+
+
+def test_camera_division_is_exact(tmp_path):
+    """camera_ray (csrc/device_common.cuh) forms (px + sx) / width from the
+    host's RN(1/width) and one fma correction; every width below 2^16 with
+    random and edge numerators must give the IEEE quotient."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = str(tmp_path / "div_check")
+    subprocess.run(["gcc", "-O2", "-mfma", "-ffp-contract=off",
+                    os.path.join(root, "tools", "div_check.c"), "-o", exe, "-lm"], check=True)
+    out = subprocess.run([exe, "300"], capture_output=True, text=True)
+    assert out.returncode == 0, out.stdout
+    assert out.stdout.startswith("0 mismatches")
