@@ -492,6 +492,8 @@ int bhrt_ctx_set_scene(bhrt_ctx* c, const bhrt_scene* s, bhrt_status_info* info)
     k.tan_half_x = k.tan_half_y * aspect;
     k.inv_width = 1.0 / s->width;  // camera_ray: (px + sx) / width by reciprocal + fma correction
     k.inv_height = 1.0 / s->height;
+    k.inv_spp = 1.0 / s->spp;
+    k.div_magic = s->width >= 2 ? ~0ull / static_cast<unsigned long long>(s->width) + 1ull : 0ull;
     k.width = s->width;
     k.height = s->height;
     k.spp = s->spp;

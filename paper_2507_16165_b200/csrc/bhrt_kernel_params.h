@@ -32,6 +32,8 @@ struct KParams {
     double forward[3], right[3], up[3];
     double tan_half_x, tan_half_y;
     double inv_width, inv_height;  // RN(1/width), RN(1/height)
+    double inv_spp;                // 1.0 / spp (render.cpp:42)
+    unsigned long long div_magic;  // floor(2^64 / width) + 1 for width >= 2, else 0 (sample_of row division)
     int32_t width, height, spp;
     int32_t pad0;
     uint64_t seed;

@@ -206,7 +206,10 @@ __device__ __forceinline__ SampleId sample_of(const KParams& p, long long i) {
     }
     int j;
     if (pix < 0x7fffffffLL) {  // 32-bit division when it fits (it does for 8K frames)
-        j = (int)((unsigned)pix / (unsigned)p.width);
+        // pix / width as the high word of pix * (floor(2^64 / width) + 1):
+        // exact for pix < 2^31, width < 2^33 (the excess pix e / 2^64, e <= 1,
+        // stays below 1 / width); width 1 has no 64-bit magic (div_magic = 0)
+        j = p.div_magic ? (int)__umul64hi((unsigned long long)pix, p.div_magic) : (int)pix;
     } else {
         j = (int)(pix / p.width);
     }
@@ -326,8 +329,8 @@ __device__ static BHRT_INL_SHADE void shade_sample(const KParams& p, int obj, in
 }
 
 // render.cpp:42-48: inv = 1/spp, round-half-away-from-zero, clamp to [0,255].
-__device__ __forceinline__ void store_pixel(uint8_t* o, const double acc[3], int spp) {
-    const double inv = 1.0 / spp;
+__device__ __forceinline__ void store_pixel(uint8_t* o, const double acc[3], double inv) {
+    // inv = 1.0 / spp, formed once on the host (KParams::inv_spp)
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
         const double scaled = round(acc[c] * inv * 255.0);
@@ -388,7 +391,7 @@ __device__ __forceinline__ void finish_sample(const KParams& p, bool valid, cons
             atomicMin(&p.stats[3], (unsigned long long)id.y * p.width + id.x);  // image order
             o[0] = o[1] = o[2] = 0;
         } else {
-            store_pixel(o, acc, p.spp);
+            store_pixel(o, acc, p.inv_spp);
         }
     }
 }

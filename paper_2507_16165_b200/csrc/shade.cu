@@ -36,7 +36,7 @@ __global__ void __launch_bounds__(256) shade_kernel(const __grid_constant__ KPar
         o[0] = o[1] = o[2] = 0;
         return;
     }
-    store_pixel(o, acc, p.spp);
+    store_pixel(o, acc, p.inv_spp);
 }
 
 void launch_reference(const KParams& p, cudaStream_t st);

@@ -219,3 +219,18 @@ def test_camera_division_is_exact(tmp_path):
     out = subprocess.run([exe, "300"], capture_output=True, text=True)
     assert out.returncode == 0, out.stdout
     assert out.stdout.startswith("0 mismatches")
+
+
+def test_row_division_magic_is_exact():
+    """sample_of (csrc/device_common.cuh) divides the packed pixel index by
+    the width as umul64hi(pix, floor(2^64 / width) + 1) (KParams::div_magic);
+    exact for every pix < 2^31 (edges of each quotient, random) and width."""
+    rng = np.random.default_rng(3)
+    widths = list(range(2, 5000)) + [int(w) for w in rng.integers(5000, 1 << 20, 3000)] + [65535, 65536, 7680]
+    for d in widths:
+        m = (2**64 - 1) // d + 1
+        top = (2**31 - 1) // d
+        ns = {0, d - 1, d, 2**31 - 1, top * d, top * d - 1}
+        ns.update(int(x) for x in rng.integers(0, 2**31 - 1, 20))
+        for n in ns:
+            assert (n * m) >> 64 == n // d, (n, d)
