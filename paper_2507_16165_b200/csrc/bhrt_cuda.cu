@@ -581,6 +581,8 @@ int bhrt_ctx_set_scene(bhrt_ctx* c, const bhrt_scene* s, bhrt_status_info* info)
         k.table_ns = s->table_samples;
         k.table_b_max = s->table_b_max;
         k.table_dpsi = s->table_dpsi;
+        k.inv_table_b_max = 1.0 / s->table_b_max;
+        k.inv_table_dpsi = 1.0 / s->table_dpsi;
         const size_t E = static_cast<size_t>(s->table_entries);
         if (!c->has_table || std::memcmp(key, c->table_key, sizeof key) != 0) {
             if (c->tab_smp.ensure(E * s->table_samples * 2) || c->tab_ends.ensure(E * 4) ||

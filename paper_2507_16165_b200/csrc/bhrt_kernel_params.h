@@ -93,6 +93,7 @@ struct KParams {
     const double* tab_psi0;
     int32_t table_entries, table_ns;
     double table_b_max, table_dpsi;
+    double inv_table_b_max, inv_table_dpsi;  // RN(1/.) from the host (exact quotients: table.cu div_by)
     // outputs
     bhrt_ray_record* records;   // n_rows * width * spp
     uint8_t* out;               // n_rows * width * 3

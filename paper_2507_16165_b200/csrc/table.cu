@@ -39,8 +39,21 @@ struct TabView {
     const int32_t* kind;
     const int32_t* n;
     int ns;
-    double dpsi;
+    double dpsi, inv_dpsi;  // inv_dpsi = RN(1 / dpsi) from the host
 };
+
+// a / b from the host's y = RN(1/b): RN(a y) plus one Markstein fma
+// correction, the IEEE quotient when a is 0 or in [2^-900, 2^900] and b is
+// a normal constant (no intermediate under/overflow; tools/div_check.c),
+// else the division.
+__device__ __forceinline__ double div_by(double a, double b, double y) {
+    const double m = fabs(a);
+    if (m >= 0x1p-900 && m <= 0x1p900) {
+        const double q0 = a * y;
+        return fma(fma(-q0, b, a), y, q0);
+    }
+    return a / b;
+}
 
 // oracle orc_table_inbound_psi
 __device__ double inbound_psi(const TabView& T, int e, double target) {
@@ -90,7 +103,7 @@ __device__ double table_u(const TabView& T, int e, double psi) {
     const double pend = __ldg(&E[0]);
     if (kind == 1 && psi > pend) psi = 2.0 * pend - psi;
     if (psi < 0.0 || n < 1) return -1.0;
-    int j = (int)floor(psi / T.dpsi);
+    int j = (int)floor(div_by(psi, T.dpsi, T.inv_dpsi));
     double h, ua, wa, ub, wb, pa;
     if (j >= n - 1) {
         if (kind == 2 || psi > pend) return -1.0;
@@ -203,7 +216,7 @@ __global__ void bind_table_kernel(const __grid_constant__ KParams p, double* end
                                   double u0, int with_esc) {
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= p.table_entries) return;
-    TabView T{p.tab_smp, ends, p.tab_kind, p.tab_n, p.table_ns, p.table_dpsi};
+    TabView T{p.tab_smp, ends, p.tab_kind, p.tab_n, p.table_ns, p.table_dpsi, 1.0 / p.table_dpsi};
     if (with_esc) ends[4 * (size_t)e + 3] = inbound_psi(T, e, p.u_esc);
     if (psi0) psi0[e] = inbound_psi(T, e, u0);
 }
@@ -249,7 +262,7 @@ __global__ void __launch_bounds__(128, BHRT_TAB_MINB) trace_table_kernel(const _
     V3 point = mk(0.0, 0.0, 0.0);
     double phi_out = 0.0;
     if (valid) {
-        const TabView T{p.tab_smp, p.tab_ends, p.tab_kind, p.tab_n, p.table_ns, p.table_dpsi};
+        const TabView T{p.tab_smp, p.tab_ends, p.tab_kind, p.tab_n, p.table_ns, p.table_dpsi, p.inv_table_dpsi};
         const V3 origin = vld(p.cam_pos), O = vld(p.center);
         const V3 dir = camera_ray(p, id.x, id.y, id.s);
         const Basis B = plane_basis(p, dir);
@@ -296,7 +309,7 @@ __global__ void __launch_bounds__(128, BHRT_TAB_MINB) trace_table_kernel(const _
                     }
                 }
                 const int N = p.table_entries;
-                const double x = (b * (double)(N - 1)) / p.table_b_max;
+                const double x = div_by(b * (double)(N - 1), p.table_b_max, p.inv_table_b_max);
                 int ie = (int)floor(x);
                 if (ie > N - 2) ie = N - 2;
                 BHRT_ASSERT(ie >= 0 && ie + 1 < N);

@@ -1,4 +1,6 @@
-/* Pins the camera_ray division in csrc/device_common.cuh: for a = px + sx
+/* Pins the reciprocal-corrected divisions (csrc/table.cu div_by: general
+ * operands, see main) and the camera_ray division in csrc/device_common.cuh:
+ * for a = px + sx
  * (px an integer pixel index < 2^16, sx in [0, 1) a 53-bit sample offset)
  * and b = width < 2^16, with y = RN(1/b) from the host,
  *   q0 = RN(a y), q = RN(q0 + RN?(a - q0 b) y)  [two fmas]
@@ -26,8 +28,23 @@ static void check(double a, double b, double y) {
         ++bad;
     }
 }
+static double make(int emin, int emax, int ones) {
+    uint64_t m = xr() & ((1ULL << 52) - 1);
+    if (ones) m |= ((1ULL << 52) - 1) ^ (xr() & 0xff);  /* mantissas near all ones */
+    const int e = emin + (int)(xr() % (uint64_t)(emax - emin + 1));
+    const uint64_t bits = ((uint64_t)(e + 1023) << 52) | m;
+    double d;
+    memcpy(&d, &bits, 8);
+    return d;
+}
 int main(int argc, char** argv) {
     const long long per = argc > 1 ? atoll(argv[1]) : 300;
+    /* general operands (table.cu div_by): |a| in [2^-900, 2^900], b in [2^-60, 2^60] */
+    for (long long i = 0; i < 400 * per; ++i) {
+        const double b = make(-60, 60, (i & 7) == 0);
+        const double a = make(-900, 899, (i & 7) == 1) * ((i & 1) ? -1.0 : 1.0);
+        check(a, b, 1.0 / b);
+    }
     for (int w = 1; w < 65536; ++w) {
         const double b = (double)w, y = 1.0 / b;
         const double sxs[3] = {0.0, 0.5, 1.0 - 0x1p-53};
