@@ -7,6 +7,12 @@
 // event steps and escape touch. Operation order mirrors the oracle
 // (oracle/bhrt_oracle.c trace_scene / step_events / escape_dir), so records
 // are bit-identical up to libdevice transcendentals outside the step.
+// The shading is called out of line in this kernel: it keeps its code out
+// of the step loop's instruction stream (config 2: 7.72 -> 7.64 ms); the
+// table kernel keeps it inline (config 3: 2.32 vs 2.36 ms out of line).
+#ifndef BHRT_INL_SHADE
+#define BHRT_INL_SHADE __noinline__
+#endif
 #include "device_common.cuh"
 
 namespace bhrt_b200 {
