@@ -6,6 +6,10 @@
 // build) and glibc's hypot restated, so window states are bit-identical to
 // the reference; only pow() (step-hint only) and sin/cos (last chord) may
 // differ by ulps (libdevice vs glibc).
+// Shading out of line here too (1080p sky-only: 95.8 -> 95.2 ms).
+#ifndef BHRT_INL_SHADE
+#define BHRT_INL_SHADE __noinline__
+#endif
 #include "device_common.cuh"
 
 namespace bhrt_b200 {
