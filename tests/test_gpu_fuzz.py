@@ -80,3 +80,20 @@ def test_random_reference_mode_scene_matches_compiled_reference(seed):
         assert rc == 0
         d = np.abs(g - rimg.astype(int))
         assert d.max() <= 1 and (d > 0).mean() <= 0.001
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_random_table_mode_scene_matches_oracle(seed):
+    """Approximate mode (b-table build on the GPU, per-frame bind, lookup)
+    on random cameras, disks, table sizes and b ranges: same contract as the
+    direct modes against the oracle's table."""
+    rng = np.random.default_rng(700 + seed)
+    sb = scenes.config(3, int(rng.integers(24, 64)), int(rng.integers(14, 36)))
+    sb.set(cam_pos=scenes.inclined_camera(rng.uniform(12.0, 45.0), rng.uniform(20.0, 160.0),
+                                          rng.uniform(0.0, 2 * math.pi)),
+           vertical_fov=math.radians(rng.uniform(30.0, 90.0)),
+           spp=int(rng.choice([1, 2, 4])), seed=int(rng.integers(1, 1 << 30)),
+           disk_enabled=int(rng.random() < 0.8), disk_r_in=rng.uniform(3.0, 8.0),
+           disk_r_out=rng.uniform(10.0, 35.0), table_entries=int(rng.choice([2000, 5000, 9000])),
+           table_b_max=float(rng.choice([30.0, 50.0, 80.0])))
+    compare(sb)
