@@ -32,7 +32,7 @@ constexpr float kWinMargin = 5e-4f;  // fp32 window slack (rad); windows only cu
 
 struct SceneSm {
     float4 sph[kSphSm];  // (cx, cy, cz, r + fp32 slack) relative to the hole: cull prefilter
-    double e1[3][kBlock], e2[3][kBlock], n[3][kBlock];
+    double e2[3][kBlock], n[3][kBlock];  // e1 is the per-frame KParams::cam_e1
     double sigma[kBlock], energy[kBlock], next_disk[kBlock];
     float lo[kSlots][kBlock], hi[kSlots][kBlock];   // angular window (unwrapped phi)
     float rlo[kSlots][kBlock], rhi[kSlots][kBlock]; // radial extent of the circle
@@ -193,8 +193,8 @@ struct Hit {
 
 // Unit disk line in plane coordinates and world space (oracle ray_events_setup
 // values, same operations), formed only when a disk crossing lands in the annulus.
-__device__ __forceinline__ void disk_line(const SceneSm& sm, int t, double& dlx, double& dly, V3& Lw) {
-    const V3 n = ld3(sm.n, t), e1 = ld3(sm.e1, t), e2 = ld3(sm.e2, t);
+__device__ __forceinline__ void disk_line(const KParams& p, const SceneSm& sm, int t, double& dlx, double& dly, V3& Lw) {
+    const V3 n = ld3(sm.n, t), e1 = vld(p.cam_e1), e2 = ld3(sm.e2, t);
     const V3 L = mk(-n.z, 0.0, n.x);
     const double nl = norm(L);
     dlx = dot(L, e1) / nl;
@@ -251,7 +251,7 @@ __device__ BHRT_INL_SPH bool sphere_search(const KParams& p, const SceneSm& sm, 
         }
         j1 = min(j1, best_j);
         if (j0 > j1) continue;
-        const V3 e1 = ld3(sm.e1, t), e2 = ld3(sm.e2, t), n = ld3(sm.n, t);
+        const V3 e1 = vld(p.cam_e1), e2 = ld3(sm.e2, t), n = ld3(sm.n, t);
         const V3 c = sphere_c(p, k);
         const double r = __ldg(&p.spheres[k].radius);
         const double dn = dot(c, n);
@@ -389,7 +389,7 @@ __device__ BHRT_INL_EVT bool step_events(const KParams& p, SceneSm& sm, int t, d
     if (act || test_all) {
         sph_hit = sphere_search(p, sm, t, pa, h, ua, ub, cu, act, nc, bsph, bqx, bqy);
         if (sph_hit) {
-            const V3 e1 = ld3(sm.e1, t), e2 = ld3(sm.e2, t);
+            const V3 e1 = vld(p.cam_e1), e2 = ld3(sm.e2, t);
             hit.point = add(vld(p.center), add(scl(e1, bqx), scl(e2, bqy)));
         }
 #ifdef BHRT_COUNTERS
@@ -400,7 +400,7 @@ __device__ BHRT_INL_EVT bool step_events(const KParams& p, SceneSm& sm, int t, d
     if (disk_hit) {
         double ux, uy;
         V3 Lw;
-        disk_line(sm, t, ux, uy, Lw);
+        disk_line(p, sm, t, ux, uy, Lw);
         if (sph_hit) {
             const double dlx = sigma * ux, dly = sigma * uy;
             if (bqx * dly - bqy * dlx > 0.0)
@@ -460,7 +460,7 @@ __device__ __forceinline__ V3 tangent_dir(V3 e1, V3 e2, double phi, double u, do
 // step (Hermite + 2 Newton iterations, u' from the first integral).
 __device__ BHRT_INL_ESC V3 escape_dir(const KParams& p, SceneSm& sm, int t, bool has_step, double pa,
                                       double ua, double wa, double pb, double ub, double wb) {
-    const V3 e1 = ld3(sm.e1, t), e2 = ld3(sm.e2, t);
+    const V3 e1 = vld(p.cam_e1), e2 = ld3(sm.e2, t);
     if (!has_step || !(ua > p.u_esc)) return tangent_dir(e1, e2, pb, ub, wb);
     const double u_esc = p.u_esc;
     const double h = pb - pa;
@@ -548,7 +548,6 @@ __global__ void __launch_bounds__(kBlock, BHRT_SCENE_MINB) trace_scene_kernel(co
             H = radial_scene(p, origin, dir, cap ? r0 - 2.0 * p.mass : p.escape_radius, cap);
         } else {
             const V3 nrm = cross(B.e1, B.e2);
-            st3(sm.e1, t, B.e1);
             st3(sm.e2, t, B.e2);
             st3(sm.n, t, nrm);
             double u, w;
