@@ -82,6 +82,10 @@ struct HintState {
 // the device pow is skipped; otherwise the exact double is formed.
 __device__ __forceinline__ double window_h0(const HintState& hs, double dphi) {
     if (!hs.pending) return dphi;
+    // err^2 <= 1e-12: err^-0.14 >= 6.9, pprev >= 1e-4^0.08 = 0.4786, so the
+    // factor is >= 2.98 (or the clamp 5) and the hint >= 2.98 h_try; when
+    // 2.9 h_try already covers dphi no pow is needed (most far-field windows)
+    if (hs.err2 <= 1e-12 && 2.9 * hs.h_try >= dphi * 1.00001) return dphi;
     if (hs.err2 >= 0.0 && hs.err2 <= 1.0 + 0x1p-52) {
         // err^2 <= 1e-30: err^-0.14 >= 126, pprev >= 1e-4^0.08 = 0.48, so the
         // factor is clamped to exactly 5 (also for err = 0: pow -> inf)
