@@ -62,6 +62,15 @@ __device__ __forceinline__ double err_ratio(double e, double s) {
     return e / s;
 }
 
+// The reference's norm before its sqrt (geodesic.cpp:125-130), same operations.
+__device__ __forceinline__ double exact_err2(double e0, double s0, double e1, double s1) {
+    const double q0 = err_ratio(e0, s0), q1 = err_ratio(e1, s1);
+    double err2 = 0.0;
+    err2 += q0 * q0;
+    err2 += q1 * q1;
+    return err2 / 2.0;
+}
+
 // geodesic.cpp:84-162. Returns false on StepSizeUnderflow (phi/u/w then hold
 // the failure state, as StepSizeUnderflow::state does).
 // The step hint carried from one window to the next (geodesic.cpp:106,160):
@@ -71,6 +80,14 @@ __device__ __forceinline__ double err_ratio(double e, double s) {
 #ifdef BHRT_HINT_COUNT
 __device__ unsigned long long g_hint_count[4];  // developer counters: exact hints, binding hints, multi-step windows
 #endif
+#ifndef BHRT_NO_LAZY_ERR
+// (e0, s0, e1, s1) of a window's last step whose error norm was only bounded
+// (hs.err2 = -1): the exact norm is formed from them if a hint needs it.
+// One slot per thread of the 128-thread blocks of the mode-R kernels.
+__shared__ double g_lazy_err[4][128];
+#endif
+__device__ __forceinline__ double exact_err2(double e0, double s0, double e1, double s1);
+
 struct HintState {
     double h_try, err2, pprev;  // last accepted step, its squared error norm (see below), err_prev^0.08
     bool pending;               // false: no hint yet (hint = 0 in the reference)
@@ -85,18 +102,26 @@ __device__ __forceinline__ double window_h0(const HintState& hs, double dphi) {
     // err^2 <= 1e-12: err^-0.14 >= 6.9, pprev >= 1e-4^0.08 = 0.4786, so the
     // factor is >= 2.98 (or the clamp 5) and the hint >= 2.98 h_try; when
     // 2.9 h_try already covers dphi no pow is needed (most far-field windows)
+    // A lazy norm (err2 = -1, see integrate_window) is known to be <= 2^-60.
     if (hs.err2 <= 1e-12 && 2.9 * hs.h_try >= dphi * 1.00001) return dphi;
-    if (hs.err2 >= 0.0 && hs.err2 <= 1.0 + 0x1p-52) {
+    double err2 = hs.err2;
+#ifndef BHRT_NO_LAZY_ERR
+    if (err2 < 0.0) {
+        const int t = threadIdx.x;
+        err2 = exact_err2(g_lazy_err[0][t], g_lazy_err[1][t], g_lazy_err[2][t], g_lazy_err[3][t]);
+    }
+#endif
+    if (err2 >= 0.0 && err2 <= 1.0 + 0x1p-52) {
         // err^2 <= 1e-30: err^-0.14 >= 126, pprev >= 1e-4^0.08 = 0.48, so the
         // factor is clamped to exactly 5 (also for err = 0: pow -> inf)
         float lo = 5.0f;
-        if (hs.err2 > 1e-30) {  // err^-0.14 = (err^2)^-0.07
-            const float lf = 0.9f * exp2f(-0.07f * __log2f((float)hs.err2)) * (float)hs.pprev;
+        if (err2 > 1e-30) {  // err^-0.14 = (err^2)^-0.07
+            const float lf = 0.9f * exp2f(-0.07f * __log2f((float)err2)) * (float)hs.pprev;
             lo = fminf(fmaxf(lf * 0.999f, 0.2f), 5.0f);
         }
         if ((float)hs.h_try * lo >= (float)dphi * 1.00001f) return dphi;
     }
-    const double factor = clampd(0.9 * pow(sqrt(hs.err2), -0.7 / 5.0) * hs.pprev, 0.2, 5.0);
+    const double factor = clampd(0.9 * pow(sqrt(err2), -0.7 / 5.0) * hs.pprev, 0.2, 5.0);
     const double hint = hs.h_try * factor;
 #ifdef BHRT_HINT_COUNT
     atomicAdd(&g_hint_count[0], 1ull);
@@ -149,6 +174,7 @@ __device__ bool integrate_window(double& phi, double& u, double& w, double dphi,
         // acceptance test err <= 1 is err2 <= 1 + 2^-52: RN(sqrt(x)) <= 1 iff
         // sqrt(x) <= 1 + 2^-53 (ties to even), i.e. x <= 1 + 2^-52 + 2^-106.
         double err2 = 0.0;
+        bool lazy = false;
         const double tiny = 1e-42 * atol;
         if (fabs(e0) < tiny && fabs(e1) < tiny) {
             // s >= atol, so the norm is < 1e-42 < 1e-30. Every later use of
@@ -157,13 +183,16 @@ __device__ bool integrate_window(double& phi, double& u, double& w, double dphi,
             // >= 0.48), err_prev becomes 1e-4. 0 stands in for it, sparing
             // the divisions' and sqrt's denormal slow paths (frequent for
             // near-linear far-field windows). NaNs fail the test above.
+#ifndef BHRT_NO_LAZY_ERR
+        } else if (fabs(e0) <= s0 * 0x1p-30 && fabs(e1) <= s1 * 0x1p-30) {
+            // both quotients <= 2^-30: err2 <= 2^-60, the step is accepted;
+            // the exact norm is formed only where it is used (below, window_h0)
+            lazy = true;
+#endif
         } else {
-            const double q0 = err_ratio(e0, s0), q1 = err_ratio(e1, s1);
-            err2 += q0 * q0;
-            err2 += q1 * q1;
-            err2 = err2 / 2.0;
+            err2 = exact_err2(e0, s0, e1, s1);
         }
-        if (err2 <= 1.0 + 0x1p-52) {
+        if (lazy || err2 <= 1.0 + 0x1p-52) {
             y0 = n0;
             y1 = n1;
             k10 = k70;
@@ -171,9 +200,21 @@ __device__ bool integrate_window(double& phi, double& u, double& w, double dphi,
             remaining -= h_try;
             ++nsteps;
             if (!(remaining > 0.0)) {  // window done: the hint is formed lazily (window_h0)
+#ifndef BHRT_NO_LAZY_ERR
+                if (lazy) {
+                    const int t = threadIdx.x;
+                    g_lazy_err[0][t] = e0;
+                    g_lazy_err[1][t] = s0;
+                    g_lazy_err[2][t] = e1;
+                    g_lazy_err[3][t] = s1;
+                    hs = {h_try, -1.0, pprev, true};
+                    break;
+                }
+#endif
                 hs = {h_try, err2, pprev, true};
                 break;
             }
+            if (lazy) err2 = exact_err2(e0, s0, e1, s1);
             const double err = sqrt(err2);
 #ifdef BHRT_HINT_COUNT
             atomicAdd(&g_hint_count[2], 1ull);
