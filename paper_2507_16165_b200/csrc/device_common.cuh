@@ -108,6 +108,14 @@ __device__ __forceinline__ double hypot_kernel(double ax, double ay) {
     return h;
 }
 __device__ inline double glibc_hypot(double x, double y) {
+    {  // the common case first: finite, unscaled, neither term negligible —
+       // exactly the branch of the full logic below that ends in hypot_kernel
+       // (NaN/inf fail these comparisons and take the full logic). Mode R
+       // 1080p sky-only: 84.6 -> 83.0 ms.
+        const double fx = fabs(x), fy = fabs(y);
+        const double hi = fx < fy ? fy : fx, lo = fx < fy ? fx : fy;
+        if (hi <= 0x1p+511 && lo >= 0x1p-511 && lo > hi * 0x1p-54) return hypot_kernel(hi, lo);
+    }
     if (!isfinite(x) || !isfinite(y)) {
         if (isinf(x) || isinf(y)) return CUDART_INF;
         return x + y;
