@@ -5,12 +5,21 @@
 
 A step = one full frame of BASELINE.json configs[C] (default C=2: 3840x2160,
 4 jittered spp, disk + 64 spheres, RKF45 tol 1e-9) rendered by all ranks
-(cyclic row tiles) and gathered to rank 0 over NCCL. Prints ONE JSON line on
-rank 0. Metric: Mrays/s (rays = pixels x spp), whole job.
+(cyclic row tiles). With N > 1 every rank's kernel stores its rows straight
+into rank 0's image over CUDA-IPC peer memory (NVLink/NVSwitch), completion
+by a stream-ordered NCCL all-reduce (an NCCL gather + unshuffle if the image
+cannot be mapped). Prints ONE JSON line on rank 0. Metric: Mrays/s (rays =
+pixels x spp), whole job.
+
+--gpus N without a torchrun environment re-launches itself under
+torch.distributed.run with N ranks (one per GPU); it exits non-zero, without
+timing anything, when fewer than N GPUs are visible.
 
 --impl reference times the CPU implementation of the same workload on the
-host cores (rank 0 only): the oracle port of the full scene (the reference
-itself cannot render disk/spheres/RKF45 — SPEC.md:14,171), kind "port".
+host cores (rank 0 only): the oracle port of the full scene on the same full
+frame (the reference itself cannot render disk/spheres/RKF45 —
+SPEC.md:14,171), kind "port"; beside it the compiled reference's own code on
+the sky-only projection through its own harness (run_strong_scaling).
 """
 from __future__ import annotations
 
@@ -84,6 +93,15 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(mhz)}
 
 
+def hbm_peak() -> float:
+    """Measured copy bandwidth (MEASURED_PEAKS.json, driver-written), else the
+    B200_PROFILING.md fallback."""
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        return 7000.0
+
+
 # ---------------------------------------------------------------- CPU legs
 def cpu_port_rows(scene, rows_sel, threads):
     """Render the selected rows with the oracle's pthread row queue."""
@@ -111,35 +129,44 @@ def centre_band(height: int, rows: int):
     return r0, min(height, r0 + rows)
 
 
-def reference_sky_only(scene, rows: int, threads: int):
+def lattice(width: int, height: int, nx: int = 96, ny: int = 64):
+    """A cyclic lattice over the whole frame: ny rows x nx columns, evenly
+    spaced (pixel centres of an ny x nx grid laid over the image)."""
+    xs = [int((i + 0.5) * width / nx) for i in range(min(nx, width))]
+    ys = [int((j + 0.5) * height / ny) for j in range(min(ny, height))]
+    return [(x, y) for y in ys for x in xs]
+
+
+def reference_sky_only(scene, threads: int, repeats: int = 5, nx: int = 96, ny: int = 64):
     """The compiled reference (oracle/_ref) on the sky-only projection of the
-    workload (its own render_rows)."""
+    workload, timed by its own harness: run_strong_scaling(scene, {threads},
+    repeats) (bench.cpp:59-73, mean of 5 as PAPER.md:265) with a RenderRunner
+    that shades a 64-row x 96-column lattice of the frame's pixels through
+    the reference's shade_pixel on `threads` threads."""
     import ctypes as C
-    import numpy as np
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     from oracle_lib import have_ref, ref
     from paper_2507_16165_b200 import scenes
-    from paper_2507_16165_b200.abi import StatusInfo
     if not have_ref():
         return None
     proj = scenes.sky_only_projection(scene)
-    r0, r1 = centre_band(proj.s.height, rows)
-    out = np.zeros((r1 - r0) * proj.s.width * 3, np.uint8)
-    info = StatusInfo()
-    t0 = time.perf_counter()
-    rc = ref().ref_render_rows(C.byref(proj.s), r0, r1, threads,
-                               out.ctypes.data_as(C.POINTER(C.c_uint8)), C.byref(info))
-    dt = time.perf_counter() - t0
-    if rc:
+    pts = lattice(proj.s.width, proj.s.height, nx, ny)
+    px = (C.c_int * len(pts))(*[p[0] for p in pts])
+    py = (C.c_int * len(pts))(*[p[1] for p in pts])
+    mean = ref().ref_strong_scaling_pixels_mean(C.byref(proj.s), threads, repeats, px, py, len(pts))
+    if not mean > 0:
         return None
-    rays = (r1 - r0) * proj.s.width * proj.s.spp
-    return {"value": rays / dt / 1e6, "unit": "Mrays/s", "cores": threads, "kind": "reference",
-            "sample": f"oracle/_ref render_rows (the reference's own code), sky-only projection "
-                      f"of the workload (DOPRI5 eps=0.05 windows, checker baked into a 2048x1024 "
-                      f"PPM), rows [{r0},{r1}) = {rays} rays, {dt:.1f} s"}
+    rays = len(pts) * proj.s.spp
+    return {"value": rays / mean / 1e6, "unit": "Mrays/s", "cores": threads, "kind": "reference",
+            "sample": f"oracle/_ref (the reference's own code) on the sky-only projection of the "
+                      f"workload (DOPRI5 eps=0.05 windows, checker baked into a 2048x1024 PPM): "
+                      f"run_strong_scaling(scene, {{{threads}}}, {repeats}) mean wall time, its "
+                      f"RenderRunner shading a {ny}-row x {nx}-column pixel lattice of the "
+                      f"{proj.s.width}x{proj.s.height} frame ({rays} rays/run) with shade_pixel",
+            "seconds_per_run": mean}
 
 
-def measure_secondary(device: int, reps: int = 3, rank: int = 0, world: int = 1) -> dict:
+def measure_secondary(device: int, peak: float, reps: int = 3, rank: int = 0, world: int = 1) -> dict:
     """Device-timed Mrays/s of configs 0, 1, 3 (scene resident, best of
     `reps` after one warm-up) and config 4's whole 120-frame orbit (frames/s,
     wall clock, per-frame scene upload + cull table included; with N ranks
@@ -148,9 +175,10 @@ def measure_secondary(device: int, reps: int = 3, rank: int = 0, world: int = 1)
     import torch
     import torch.distributed as dist
 
-    from paper_2507_16165_b200 import render, scenes
+    from paper_2507_16165_b200 import render, roofline, scenes
     out = {}
     ctx = render.Context(device)
+    ctx.set_timing(True)
     st = torch.cuda.current_stream()
     for idx in (0, 1, 3) if rank == 0 else ():
         sb = scenes.config(idx)
@@ -159,6 +187,7 @@ def measure_secondary(device: int, reps: int = 3, rank: int = 0, world: int = 1)
         setup_s = time.perf_counter() - t0
         buf = torch.empty(sb.s.width * sb.s.height * 3, dtype=torch.uint8, device="cuda")
         best = None
+        kern = None
         for r in range(reps + 1):
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
@@ -169,10 +198,29 @@ def measure_secondary(device: int, reps: int = 3, rank: int = 0, world: int = 1)
             ms = e0.elapsed_time(e1)
             if r > 0 and (best is None or ms < best):
                 best = ms
+                kern = ctx.kernel_ms()[0]
         rays = sb.s.width * sb.s.height * sb.s.spp
-        out[f"config{idx}"] = {"ms": best, "Mrays/s": rays / best / 1e3,
-                               "steps_per_ray": ctx.stats()["steps"] / rays,
-                               "set_scene_s": setup_s, "size": [sb.s.width, sb.s.height, sb.s.spp]}
+        stats = ctx.stats()
+        line = {"ms": best, "kernel_ms": kern, "Mrays/s": rays / best / 1e3,
+                "steps_per_ray": stats["steps"] / rays,
+                "set_scene_s": setup_s, "size": [sb.s.width, sb.s.height, sb.s.spp]}
+        if idx == 3:
+            # table mode: no integration; bound by the latency of its table
+            # gathers (L1/L2). Algorithmic bytes = roofline.table_bytes
+            # (per-sample lookups + per-event orbit evaluations + RGB8 out)
+            nbytes = roofline.table_bytes(sb, stats)
+            line["steps_per_ray"] = None
+            line["orbit_evals_per_ray"] = stats["steps"] / rays
+            line["roofline"] = {"bound": "latency (table gathers)", "algorithmic_bytes": nbytes,
+                                "achieved_GBps": nbytes / (kern * 1e-3) / 1e9, "unit": "GB/s",
+                                "hbm_peak_GBps": hbm_peak(),
+                                "frac_of_hbm": nbytes / (kern * 1e-3) / 1e9 / hbm_peak()}
+        else:
+            fl = roofline.launch_flops(sb, stats)
+            line["roofline"] = {"bound": "fp64", "flops_per_launch": fl,
+                                "achieved": fl / (kern * 1e-3) / 1e12, "peak": peak,
+                                "unit": "TFLOP/s", "frac": fl / (kern * 1e-3) / 1e12 / peak}
+        out[f"config{idx}"] = line
     frames = 120
     sb0 = scenes.config(4, frame=0)
     buf = torch.empty(sb0.s.width * sb0.s.height * 3, dtype=torch.uint8, device="cuda")
@@ -192,24 +240,33 @@ def measure_secondary(device: int, reps: int = 3, rank: int = 0, world: int = 1)
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
+    flops4 = 0.0
     for f, sb in enumerate(mine):
         c = ctxs[f % 2]
         c.set_scene(sb)
         c.render_async(bufs[f % 2].data_ptr(), stream=st.cuda_stream)
         if f > 0:
             ctxs[(f - 1) % 2].finish()
+            flops4 += roofline.launch_flops(mine[f - 1], ctxs[(f - 1) % 2].stats())
     if mine:
         ctxs[(len(mine) - 1) % 2].finish()
+        flops4 += roofline.launch_flops(mine[-1], ctxs[(len(mine) - 1) % 2].stats())
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
+    tdt = torch.tensor([dt, flops4], device="cuda", dtype=torch.float64)
     if world > 1:
-        tdt = torch.tensor([dt], device="cuda", dtype=torch.float64)
-        dist.all_reduce(tdt, op=dist.ReduceOp.MAX)
-        dt = float(tdt.item())
+        tmax = tdt[:1].clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tdt, op=dist.ReduceOp.SUM)
+        dt, flops4 = float(tmax.item()), float(tdt[1].item())
     ctx2.close()
     out["config4"] = {"frames": frames, "seconds": dt, "frames/s": frames / dt,
                       "Mrays/s": frames * sb0.s.width * sb0.s.height * sb0.s.spp / dt / 1e6,
                       "size": [sb0.s.width, sb0.s.height, sb0.s.spp], "n_gpus": world,
+                      "roofline": {"bound": "fp64", "flops": flops4,
+                                   "achieved": flops4 / dt / 1e12 / world, "peak": peak,
+                                   "unit": "TFLOP/s per GPU", "frac": flops4 / dt / 1e12 / world / peak,
+                                   "note": "whole orbit incl. per-frame host setup (wall clock)"},
                       "note": "frames sharded f mod N; whole-box rate = frames / slowest rank"}
     if rank != 0:
         ctx.close()
@@ -275,8 +332,14 @@ def measure_secondary(device: int, reps: int = 3, rank: int = 0, world: int = 1)
     ctx.finish()
     ms = e0.elapsed_time(e1)
     rays = proj.s.width * proj.s.height * proj.s.spp
-    out["modeR_sky_only"] = {"ms": ms, "Mrays/s": rays / ms / 1e3,
-                             "windows_per_ray": ctx.stats()["steps"] / rays,
+    stR = ctx.stats()
+    flR = roofline.launch_flops(proj, stR)
+    kR = ctx.kernel_ms()[0]
+    out["modeR_sky_only"] = {"ms": ms, "kernel_ms": kR, "Mrays/s": rays / ms / 1e3,
+                             "windows_per_ray": stR["steps"] / rays,
+                             "roofline": {"bound": "fp64", "flops_per_launch": flR,
+                                          "achieved": flR / (kR * 1e-3) / 1e12, "peak": peak,
+                                          "unit": "TFLOP/s", "frac": flR / (kR * 1e-3) / 1e12 / peak},
                              "size": [proj.s.width, proj.s.height, proj.s.spp],
                              "note": "trace_reference_kernel (reference algorithm, bit-identical "
                                      "window arithmetic) on the full sky-only projection; compare "
@@ -287,29 +350,38 @@ def measure_secondary(device: int, reps: int = 3, rank: int = 0, world: int = 1)
 
 # ---------------------------------------------------------------- arms
 def run_reference_arm(args):
+    """The CPU implementation of the path on this box's host cores (rank 0
+    only): the oracle port (C, pthreads) renders the same full frame as our
+    arm each step. The scene is built with the oracle's own sphere generator,
+    so no product library is loaded in this process."""
     rank, world, _ = env_rank()
     if rank != 0:
         return 0
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_lib import oracle
     from paper_2507_16165_b200 import scenes
-    scene = scenes.config(args.config)
+    scene = scenes.config(args.config, sphere_lib=oracle())
     threads = os.cpu_count() or 1
-    rows = args.ref_rows
-    band = centre_band(scene.s.height, rows)
-    for _ in range(args.warmup):
-        cpu_port_rows(scene, (band[0], band[0] + 1), threads)
+    H = scene.s.height
+    band = (0, H) if args.ref_rows is None else centre_band(H, args.ref_rows)
+    for _ in range(args.warmup):  # untimed: thread pool + caches, one centre row
+        cpu_port_rows(scene, centre_band(H, 1), threads)
     tot_rays, tot_s = 0, 0.0
-    per = []
     for _ in range(args.steps):
         rays, dt = cpu_port_rows(scene, band, threads)
         tot_rays += rays
         tot_s += dt
-        per.append(dt)
     value = tot_rays / tot_s / 1e6
-    sample = (f"oracle port (C, pthreads) of the full workload, centre rows [{band[0]},{band[1]}) "
-              f"= {tot_rays // args.steps} rays per step")
+    full = band == (0, H)
+    sample = (f"oracle port (C, pthreads) of the full workload, "
+              + (f"the whole {scene.s.width}x{H}x{scene.s.spp} frame" if full
+                 else f"rows [{band[0]},{band[1]})")
+              + f" = {tot_rays // args.steps} rays per step")
+    ref_sky = None if args.no_ref_sky else reference_sky_only(scene, threads)
     line = {
         "impl": "reference", "metric": "Mrays/s", "value": value, "unit": "Mrays/s",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "n_gpus": world if "WORLD_SIZE" in os.environ else args.gpus,
+        "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * tot_s / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOADS[args.config], "width": scene.s.width,
@@ -318,19 +390,72 @@ def run_reference_arm(args):
                          "sample": sample},
         "e2e": {"value": value, "unit": "Mrays/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "reference_sky_only": ref_sky,
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-def run_ours(args):
+def dropin_e2e(scene, device: int, iters: int, flush) -> dict:
+    """The reference-facing drop-in: bhrt_cuda_render_rows (include/bhrt_cuda.h,
+    the C ABI render_shim.cpp's render_rows calls) with HOST buffers — scene
+    from host memory, pixels into a caller-owned host buffer — timed end to
+    end per call (wall clock, synchronous API)."""
     import ctypes as C
 
+    import numpy as np
+    import torch
+
+    from paper_2507_16165_b200 import native
+    from paper_2507_16165_b200.abi import StatusInfo
+    L = native.lib()
+    W, H = scene.s.width, scene.s.height
+    out = np.zeros(W * H * 3, np.uint8)  # caller-owned, pages touched once
+    devs = (C.c_int32 * 1)(device)
+    info = StatusInfo()
+
+    def call():
+        rc = L.bhrt_cuda_render_rows(scene.ptr(), 0, H, devs, 1,
+                                     out.ctypes.data_as(C.POINTER(C.c_uint8)), out.nbytes, None,
+                                     C.byref(info))
+        native.check(rc, info)
+
+    call()
+    call()
+    ms = []
+    for _ in range(iters):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        call()
+        ms.append((time.perf_counter() - t0) * 1e3)
+    return {"ms": ms, "image": out}
+
+
+def self_launch(args) -> int:
+    """--gpus N outside torchrun: re-launch under torch.distributed.run with N
+    ranks, or refuse (non-zero, nothing timed) when fewer GPUs are visible."""
+    import torch
+    n = torch.cuda.device_count()
+    if n < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} requested but only {n} CUDA device(s) are visible; "
+              f"refusing to time fewer GPUs than requested", file=sys.stderr, flush=True)
+        return 2
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def run_ours(args):
     import torch
     import torch.distributed as dist
 
     from paper_2507_16165_b200 import native, roofline, scenes
-    from paper_2507_16165_b200.abi import Scene, Sphere
     from paper_2507_16165_b200.parallel import FrameRenderer
 
     rank, world, local = env_rank()
@@ -393,6 +518,7 @@ def run_ours(args):
     # ---- e2e through the public API: H2D scene, render, gather, D2H image
     e2e_ms = []
     for i in range(max(2, args.steps) + 1):
+        flush.zero_()
         torch.cuda.synchronize()
         barrier()
         t0 = time.perf_counter()
@@ -405,10 +531,23 @@ def run_ours(args):
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = total_rays / (float(te.item()) * 1e-3) / 1e6
-    h2d = C.sizeof(Scene) + C.sizeof(Sphere) * scene.s.n_spheres
-    if scene.s.sky_kind == 0 and scene.sky is not None:
-        h2d += scene.sky.nbytes
-    d2h = W * H * 3 if rank == 0 else 0
+    staged, params = fr.ctx.upload_bytes()
+    e2e_launches = fr.ctx.stats()["launches"]
+    # scene uploads + kernel parameter blocks + the counters' reset (8 x u64)
+    h2d = staged + e2e_launches * params + 64
+    d2h = (W * H * 3 if rank == 0 else 0) + 64  # the image + the counters
+    peer = fr.peer is not None
+
+    # ---- the reference-facing drop-in (C ABI, host buffers), N = 1
+    dropin = None
+    if world == 1:
+        dr = dropin_e2e(scene, local, max(3, args.steps), flush)
+        dms = sum(dr["ms"]) / len(dr["ms"])
+        same = bool((dr["image"].reshape(H, W, 3) == fr.host.numpy()).all())
+        dropin = {"value": total_rays / (dms * 1e-3) / 1e6, "unit": "Mrays/s", "ms": dms,
+                  "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                  "api": "bhrt_cuda_render_rows (C ABI; render_shim.cpp render_rows), host buffers",
+                  "image_equals_frame_renderer": same}
 
     if rank != 0:
         dist.barrier() if world > 1 else None
@@ -433,7 +572,7 @@ def run_ours(args):
     # ---- the other BASELINE.json configs (secondary lines, rank 0, this GPU)
     secondary = None
     if not args.no_secondary:
-        secondary = measure_secondary(local, rank=rank, world=world)
+        secondary = measure_secondary(local, peak, rank=rank, world=world)
 
     # ---- CPU baseline on this box's host cores (rank 0, N=1 only)
     cpu = None
@@ -443,10 +582,18 @@ def run_ours(args):
         band = centre_band(H, args.cpu_rows)
         rays, dt = cpu_port_rows(scene, band, threads)
         cpu = {"value": rays / dt / 1e6, "unit": "Mrays/s", "cores": threads, "kind": "port",
-               "sample": f"oracle port (C, pthreads) of the full workload, centre rows "
+               "sample": f"oracle port (C, pthreads) of the full workload, rows "
                          f"[{band[0]},{band[1]}) = {rays} rays, {dt:.1f} s"}
-        ref_sky = reference_sky_only(scene, args.ref_sky_rows, threads)
+        if not args.no_ref_sky:
+            ref_sky = reference_sky_only(scene, threads)
 
+    if world > 1:
+        par = (f"cyclic rows x{world}: each rank's kernel stores its rows into rank 0's image "
+               f"over CUDA-IPC peer memory (NVLink), completion by a stream-ordered NCCL "
+               f"all-reduce" if peer else
+               f"cyclic rows x{world} + NCCL gather + unshuffle on rank 0")
+    else:
+        par = "1 GPU"
     line = {
         "metric": "Mrays/s", "value": value, "unit": "Mrays/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms_max,
@@ -455,7 +602,7 @@ def run_ours(args):
         "config": {"workload": WORKLOADS[args.config], "width": W, "height": H, "spp": spp,
                    "rays_per_step": total_rays,
                    "l2": "flushed between steps (256 MiB write, outside the timed window)",
-                   "parallelism": f"cyclic rows x{world} + NCCL gather" if world > 1 else "1 GPU"},
+                   "parallelism": par},
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "fp64_pipe_active_ncu": pipe_busy,
@@ -467,7 +614,9 @@ def run_ours(args):
         "cpu_baseline": cpu,
         "reference_sky_only": ref_sky,
         "e2e": {"value": e2e_value, "unit": "Mrays/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h},
+                "d2h_bytes_per_step": d2h,
+                "api": "FrameRenderer.render (python; pinned host image)"},
+        "e2e_dropin": dropin,
         "mpixels_per_s": value / spp,  # BASELINE metric also quotes pixels/s
         "gpu_launches": stats["launches"] * args.steps if stats else None,
         "gpu_launches_per_step": stats["launches"] if stats else None,
@@ -490,17 +639,27 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=2, choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    # CPU samples: rows of the workload around the frame centre (the whole
-    # 2160-row frame is ~3 s on 16 cores for the port; the reference's own
-    # epsilon-window path is ~1e5x slower, so it gets 2 rows)
+    # CPU samples: the oracle port renders the whole frame (~2 s on 16 cores
+    # for config 2); --ref-rows N restricts the reference arm to N centre rows
     ap.add_argument("--cpu-rows", type=int, default=2160)
-    ap.add_argument("--ref-rows", type=int, default=540)
-    ap.add_argument("--ref-sky-rows", type=int, default=2)
+    ap.add_argument("--ref-rows", type=int, default=None)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-ref-sky", action="store_true",
+                    help="skip the compiled reference's sky-only lattice timing (~10 s)")
     ap.add_argument("--no-secondary", action="store_true")
     args = ap.parse_args()
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
     if args.impl == "reference":
         return run_reference_arm(args)
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is None:
+        if args.gpus > 1:
+            return self_launch(args)
+    elif int(env_world) != args.gpus:
+        print(f"bench.py: launched with WORLD_SIZE={env_world} but --gpus {args.gpus}; "
+              f"they must agree", file=sys.stderr, flush=True)
+        return 2
     return run_ours(args)
 
 

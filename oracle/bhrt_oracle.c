@@ -88,6 +88,23 @@ static int cam_setup(const bhrt_scene* s, cam_t* c) {
     return 0;
 }
 
+/* camera.cpp:49-51 before the normalisation: D = f + (2u-1) thx r + (1-2v) thy up */
+static v3 cam_dir_raw(const bhrt_scene* s, const cam_t* c, int px, int py, int sample) {
+    double sx = 0.5, sy = 0.5; /* camera.cpp:55-65 */
+    if (s->spp > 1) {
+        sx = to_unit(orc_hash_counter(s->seed, (uint64_t)px, (uint64_t)py, 2 * (uint64_t)sample));
+        sy = to_unit(orc_hash_counter(s->seed, (uint64_t)px, (uint64_t)py, 2 * (uint64_t)sample + 1));
+    }
+    const double u = (px + sx) / s->width;
+    const double v = (py + sy) / s->height;
+    return add(add(c->forward, scl(c->right, (2.0 * u - 1.0) * c->tan_half_x)),
+               scl(c->up, (1.0 - 2.0 * v) * c->tan_half_y));
+}
+
+/* Unit vector by one reciprocal (scene modes; the reference's normalized()
+ * divides three times, vec3.hpp:36-39). */
+static inline v3 unit_fast(v3 a) { const double inv = 1.0 / norm(a); return scl(a, inv); }
+
 static v3 cam_ray(const bhrt_scene* s, const cam_t* c, int px, int py, int sample) {
     double sx = 0.5, sy = 0.5; /* camera.cpp:55-65 */
     if (s->spp > 1) {
@@ -634,6 +651,8 @@ typedef struct {
     cam_t cam;
     double u_cap, u_esc, phi_max, M3;
     v3 light;
+    v3 e1;     /* scene modes: normalized(camera - center), per frame */
+    double u0; /* scene modes: 1 / |camera - center| */
     orc_table* table;  /* approximate mode: the b-table ... */
     double* psi0;      /* ... and each entry's inbound psi of the camera's u0 */
 } prep_t;
@@ -647,6 +666,11 @@ static int prep_scene(const bhrt_scene* s, prep_t* p) {
     p->phi_max = 2.0 * PI * s->max_windings;
     p->M3 = 3.0 * s->mass;
     p->light = normalized(vld(s->light_dir));
+    {   /* per-frame plane_basis / initial_conditions constants (geodesic.cpp:49-65) */
+        const v3 v = sub(vld(s->cam_pos), vld(s->center));
+        p->e1 = normalized(v);
+        p->u0 = 1.0 / norm(v);
+    }
     p->table = NULL;
     p->psi0 = NULL;
     return 0;
@@ -691,8 +715,9 @@ static void ray_events_setup(scene_ray_t* R) {
          * through O along L = n x (0,1,0); crossings are the phi-events
          * phi_L + k*pi. The hit direction alternates between +L^ and -L^. */
         const v3 L = mk(-R->n.z, 0.0, R->n.x);
-        const double nl = norm(L);
-        if (nl >= 1e-12) {
+        const double nl2 = dot(L, L);
+        if (nl2 >= 1e-24) { /* |L| >= 1e-12 */
+            const double nl = sqrt(nl2);
             const double lx = dot(L, R->e1), ly = dot(L, R->e2);
             const double pl = atan2(ly, lx);
             R->next_disk = pl > 0.0 ? pl : pl + PI;
@@ -740,6 +765,36 @@ static inline double hermite(double t, double h, double ua, double wa, double ub
     double a[4];
     hermite_coef(h, ua, wa, ub, wb, a);
     return hermite_eval(a, t);
+}
+
+/* Scene-mode ray setup (RK4 / RKF45 / TABLE; DESIGN.md §2 "Scene-mode ray
+ * setup"): the orbital frame straight from the camera's unnormalised
+ * direction D. e1 = (o - O)/|o - O| and u0 = 1/|o - O| are per-frame
+ * (geodesic.cpp:49-65 with o = the camera); with c = D.e1 and T = D - c e1,
+ * e2 = T / |T| (one reciprocal) and u0' = -(c / |T|) u0, which is the
+ * reference's -(v.d)/(r0 b) with v = r0 e1, d = D/|D|, b = r0 |T| / |D|
+ * (geodesic.cpp:57-65). The ray is radial iff |T|^2 < 1e-24 |D|^2 (the
+ * reference's |tangential| < 1e-12 for unit d, geodesic.cpp:53); only then
+ * is D normalised (radial_scene needs a unit direction). */
+typedef struct {
+    int ok;
+    v3 e2;
+    double w;
+} frame_t;
+
+static frame_t scene_frame(v3 e1, double u0, v3 D) {
+    frame_t f;
+    const double c = dot(D, e1);
+    const v3 T = sub(D, scl(e1, c));
+    const double t2 = dot(T, T);
+    f.ok = !(t2 < 1e-24 * dot(D, D));
+    f.e2 = mk(0.0, 0.0, 0.0);
+    f.w = 0.0;
+    if (!f.ok) return f;
+    const double inv = 1.0 / sqrt(t2);
+    f.e2 = scl(T, inv);
+    f.w = -((c * inv) * u0);
+    return f;
 }
 
 /* Hit tests over one accepted step (pa, ua, wa) -> (pb, ub, wb), DESIGN.md §Events.
@@ -856,7 +911,7 @@ static int step_events(scene_ray_t* R, double pa, double ua, double wa, double p
 static v3 tangent_dir(const scene_ray_t* R, double phi, double u, double w) {
     const double c = cos(phi), sn = sin(phi);
     const double tx = -u * sn - w * c, ty = u * c - w * sn;
-    return normalized(add(scl(R->e1, tx), scl(R->e2, ty)));
+    return unit_fast(add(scl(R->e1, tx), scl(R->e2, ty)));
 }
 
 /* d/dt of hermite() (t in [0,1]); h01' = -h00'. */
@@ -928,22 +983,20 @@ static int trace_scene(const bhrt_scene* s, const prep_t* P, v3 origin, v3 dir, 
     rec->steps = 0;
     rec->rejected = 0;
     rec->phi = 0.0;
-    const double o[3] = {origin.x, origin.y, origin.z}, d[3] = {dir.x, dir.y, dir.z};
-    double e1a[3], e2a[3];
-    if (!orc_plane_basis(o, d, s->center, e1a, e2a)) {
+    const frame_t F = scene_frame(P->e1, P->u0, dir); /* dir: the raw camera direction */
+    if (!F.ok) {
+        const v3 ud = normalized(dir);
         const v3 v = sub(origin, R->O);
         const double r0 = norm(v);
-        const int cap = dot(dir, sub(R->O, origin)) > 0.0;
-        radial_scene(R, origin, dir, cap ? r0 - 2.0 * s->mass : s->escape_radius, cap);
+        const int cap = dot(ud, sub(R->O, origin)) > 0.0;
+        radial_scene(R, origin, ud, cap ? r0 - 2.0 * s->mass : s->escape_radius, cap);
         return 0;
     }
-    R->e1 = vld(e1a);
-    R->e2 = vld(e2a);
+    R->e1 = P->e1;
+    R->e2 = F.e2;
     R->n = cross(R->e1, R->e2);
-    double st[3];
-    orc_initial_conditions(o, d, s->center, st);
     ray_events_setup(R);
-    double phi = 0.0, u = st[1], w = st[2];
+    double phi = 0.0, u = P->u0, w = F.w;
     double pp = 0.0, up = 0.0, wp = 0.0; /* state before the last accepted step */
     int has_step = 0;
     const double M2 = 2.0 * s->mass;
@@ -1211,20 +1264,18 @@ static int trace_table(const bhrt_scene* s, const prep_t* P, v3 origin, v3 dir, 
     rec->steps = 0;
     rec->rejected = 0;
     rec->phi = 0.0;
-    const double o[3] = {origin.x, origin.y, origin.z}, d[3] = {dir.x, dir.y, dir.z};
-    double e1a[3], e2a[3];
-    if (!orc_plane_basis(o, d, s->center, e1a, e2a)) {
+    const frame_t F = scene_frame(P->e1, P->u0, dir); /* dir: the raw camera direction */
+    if (!F.ok) {
+        const v3 ud = normalized(dir);
         const double r0 = norm(sub(origin, R->O));
-        const int cap = dot(dir, sub(R->O, origin)) > 0.0;
-        radial_scene(R, origin, dir, cap ? r0 - 2.0 * s->mass : s->escape_radius, cap);
+        const int cap = dot(ud, sub(R->O, origin)) > 0.0;
+        radial_scene(R, origin, ud, cap ? r0 - 2.0 * s->mass : s->escape_radius, cap);
         return 0;
     }
-    R->e1 = vld(e1a);
-    R->e2 = vld(e2a);
+    R->e1 = P->e1;
+    R->e2 = F.e2;
     R->n = cross(R->e1, R->e2);
-    double st[3];
-    orc_initial_conditions(o, d, s->center, st);
-    const double u0 = st[1], w0 = st[2];
+    const double u0 = P->u0, w0 = F.w;
     const double M2 = 2.0 * s->mass;
     const double energy = w0 * w0 + u0 * u0 - M2 * u0 * u0 * u0;
     /* The orbit's impact parameter is fixed by its first integral
@@ -1307,7 +1358,7 @@ static void shade_object(const bhrt_scene* s, const prep_t* P, const scene_ray_t
         }
         case BHRT_OBJ_SPHERE: {
             const bhrt_sphere* sp = &s->spheres[R->sphere];
-            const v3 nrm = dvd(sub(R->point, vld(sp->center)), sp->radius);
+            const v3 nrm = scl(sub(R->point, vld(sp->center)), 1.0 / sp->radius);
             const double lam = dmax(0.0, dot(nrm, P->light));
             const double k = s->ambient + (1.0 - s->ambient) * lam;
             for (int c = 0; c < 3; ++c) rgb[c] = sp->albedo[c] * k;
@@ -1320,7 +1371,9 @@ static void shade_object(const bhrt_scene* s, const prep_t* P, const scene_ray_t
 static int trace_sample_prepared(const bhrt_scene* s, const prep_t* P, int px, int py, int sample,
                                  bhrt_ray_record* rec, double rgb[3]) {
     const v3 origin = vld(s->cam_pos);
-    const v3 dir = cam_ray(s, &P->cam, px, py, sample);
+    /* mode R: the reference's unit ray; scene modes: the raw direction (scene_frame) */
+    const v3 dir = s->integrator == BHRT_INTEGRATOR_REFERENCE ? cam_ray(s, &P->cam, px, py, sample)
+                                                              : cam_dir_raw(s, &P->cam, px, py, sample);
     rec->sphere = -1;
     rec->point[0] = rec->point[1] = rec->point[2] = 0.0;
     rgb[0] = rgb[1] = rgb[2] = 0.0;

@@ -3,9 +3,12 @@
 // sources under /root/reference/proj (never copied into this repo) and used by
 // tests/ to pin the oracle, by tests/golden/make_golden.py to produce the
 // committed fixtures, and by bench.py's reference-arm / cpu_baseline legs.
+#include <atomic>
 #include <chrono>
 #include <cstring>
 #include <exception>
+#include <mutex>
+#include <thread>
 #include <vector>
 
 #include "bhrt/bench.hpp"
@@ -222,6 +225,46 @@ double ref_strong_scaling_mean(const bhrt_scene* s, int threads, int repeats) {
     try {
         const SceneConfig sc = to_scene(s, bg);
         const auto recs = run_strong_scaling(sc, {threads}, repeats);
+        mean = mean_wall_seconds(recs, threads);
+    } catch (const std::exception&) {
+        mean = -1.0;
+    }
+    delete bg;
+    return mean;
+}
+
+// The reference's timing harness (run_strong_scaling, bench.cpp:59-73, timed
+// at :13-22) with a RenderRunner (bench.hpp:32) that renders a SAMPLE of the
+// frame's pixels — (px[i], py[i]), i < n — through the reference's own
+// shade_pixel (render.cpp:22-49), pulled from a shared atomic counter by
+// `threads` std::threads (render_rows' dynamic queue, render.cpp:80-115, at
+// pixel granularity). Mean wall seconds of `repeats` runs; -1 on failure.
+double ref_strong_scaling_pixels_mean(const bhrt_scene* s, int threads, int repeats, const int* px,
+                                      const int* py, int n) {
+    ImageBuffer* bg = make_bg(s);
+    double mean = -1.0;
+    try {
+        const SceneConfig sc = to_scene(s, bg);
+        const RenderRunner runner = [px, py, n](const SceneConfig& scene, int workers) {
+            std::atomic<int> next{0};
+            std::exception_ptr err;
+            std::mutex mu;
+            std::vector<std::thread> pool;
+            for (int t = 0; t < workers; ++t)
+                pool.emplace_back([&] {
+                    try {
+                        for (int i = next.fetch_add(1); i < n; i = next.fetch_add(1))
+                            (void)shade_pixel(scene, px[i], py[i]);
+                    } catch (...) {  // first failure wins (render.cpp:100-104)
+                        std::lock_guard<std::mutex> g(mu);
+                        if (!err) err = std::current_exception();
+                        next.store(n);
+                    }
+                });
+            for (auto& th : pool) th.join();
+            if (err) std::rethrow_exception(err);
+        };
+        const auto recs = run_strong_scaling(sc, {threads}, repeats, BenchMode::threads, runner);
         mean = mean_wall_seconds(recs, threads);
     } catch (const std::exception&) {
         mean = -1.0;

@@ -238,6 +238,16 @@ struct bhrt_ctx {
     bool timing = false;
     bool timed = false;
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+    uint64_t upload_bytes = 0;  // host->device bytes staged by the last set_scene
+    // one-shot host-buffer path (bhrt_cuda_render_rows): row bands alternate
+    // between two render streams; each band's rows go device->pinned staging
+    // on a copy stream while later bands render; the host then places them
+    // in the caller's buffer as they land
+    cudaStream_t band_stream[2] = {nullptr, nullptr};
+    cudaStream_t copy_stream = nullptr;
+    std::vector<cudaEvent_t> band_ev;  // [2b] band b rendered, [2b+1] band b on the host
+    unsigned char* host_out = nullptr;
+    size_t host_out_cap = 0;
 };
 
 extern "C" {
@@ -445,6 +455,11 @@ void bhrt_ctx_destroy(bhrt_ctx* c) {
     if (c->render_done) cudaEventDestroy(c->render_done);
     for (auto e : c->frame_ev) cudaEventDestroy(e);
     if (c->up_stream) cudaStreamDestroy(c->up_stream);
+    for (auto st : c->band_stream)
+        if (st) cudaStreamDestroy(st);
+    if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+    for (auto e : c->band_ev) cudaEventDestroy(e);
+    if (c->host_out) cudaFreeHost(c->host_out);
     c->tab_smp.release();
     c->tab_ends.release();
     c->tab_psi0.release();
@@ -463,6 +478,10 @@ int bhrt_ctx_set_scene(bhrt_ctx* c, const bhrt_scene* s, bhrt_status_info* info)
     // render and its previous uploads (other contexts keep running)
     if (c->pending) CK(cudaEventSynchronize(c->render_done));
     CK(cudaStreamSynchronize(c->up_stream));
+    // the parameters below are rebuilt in place: until every step of the
+    // upload has succeeded the context holds no renderable scene (a failed
+    // allocation/copy must not leave a half-built KParams behind)
+    c->has_scene = false;
     KParams& k = c->kp;
     std::memset(&k, 0, sizeof k);
     k.mass = s->mass;
@@ -533,6 +552,7 @@ int bhrt_ctx_set_scene(bhrt_ctx* c, const bhrt_scene* s, bhrt_status_info* info)
     const size_t cull_bytes = cull ? sizeof(unsigned long long) * table.size() : 0;
     const size_t chk_bytes = sizeof checker;
     const size_t need = chk_bytes + sky_bytes + sph_bytes + cull_bytes;
+    c->upload_bytes = need;
     if (need > c->staging_cap) {
         if (c->staging) CK(cudaFreeHost(c->staging));
         c->staging = nullptr;
@@ -757,6 +777,61 @@ int bhrt_ctx_frame_begin(bhrt_ctx* c, void* stream, bhrt_status_info* info) {
     return 0;
 }
 
+// The reference's failure text for the lowest failing pixel (render.cpp:36-40
+// forwards e.what(): geodesic.cpp:234 "trace: inverse radius left the
+// positive domain", or StepSizeUnderflow's "adaptive step size underflow near
+// u = <u>", geodesic.hpp:72-74). The frame's kernels only flag the pixel; on
+// failure its row is traced once more with records (cold path), whose
+// failing samples carry (u, kind) in point[0..1], and the first failing
+// sample in sample order (shade_pixel's loop, render.cpp:25) names the error.
+static void failure_text(bhrt_ctx* c, int px, int py, char* out, size_t cap) {
+    std::snprintf(out, cap, "numerical failure");
+    KParams k = c->kp;
+    const size_t nrec = static_cast<size_t>(k.width) * k.spp;
+    DevBuf<bhrt_ray_record> rec;
+    DevBuf<uint8_t> img;
+    if (rec.ensure(nrec) || img.ensure(3 * static_cast<size_t>(k.width))) {
+        rec.release();
+        img.release();
+        (void)cudaGetLastError();
+        return;
+    }
+    k.row_start = py;
+    k.row_end = py + 1;
+    k.tile_rows = 1;
+    k.tile_stride = 1;
+    k.tile_offset = 0;
+    k.n_rows = 1;
+    k.records = rec.p;
+    k.out = img.p;
+    k.out_image = 0;
+    k.stats = c->stats.p;  // the frame's counters are already on the host
+    k.diag = 1;            // the diagnostic kernel instantiations
+    std::vector<bhrt_ray_record> h(k.spp);
+    int launches = 0;
+    bool ok = cudaMemcpyAsync(c->stats.p, c->host_stats + 8, 8 * sizeof(unsigned long long),
+                              cudaMemcpyHostToDevice, c->up_stream) == cudaSuccess &&
+              launch_trace(k, c->up_stream, &launches, nullptr) == 0 &&
+              cudaMemcpyAsync(h.data(), rec.p + static_cast<size_t>(px) * k.spp,
+                              sizeof(bhrt_ray_record) * k.spp, cudaMemcpyDeviceToHost,
+                              c->up_stream) == cudaSuccess &&
+              cudaStreamSynchronize(c->up_stream) == cudaSuccess;
+    rec.release();
+    img.release();
+    if (!ok) {
+        (void)cudaGetLastError();
+        return;
+    }
+    for (const bhrt_ray_record& r : h) {
+        if (r.object != -BHRT_NUMERICAL) continue;
+        if (r.point[1] == 2.0)
+            std::snprintf(out, cap, "adaptive step size underflow near u = %f", r.point[0]);
+        else
+            std::snprintf(out, cap, "trace: inverse radius left the positive domain");
+        return;
+    }
+}
+
 int bhrt_ctx_finish(bhrt_ctx* c, bhrt_status_info* info) {
     set_info(info, 0, -1, -1, "");
     if (!c) return set_info(info, BHRT_INVALID_ARGUMENT, -1, -1, "NULL context");
@@ -777,10 +852,18 @@ int bhrt_ctx_finish(bhrt_ctx* c, bhrt_status_info* info) {
     if (fail != ULLONG_MAX) {
         const int py = static_cast<int>(fail / c->kp.width);
         const int px = static_cast<int>(fail % c->kp.width);
-        char msg[96];
-        std::snprintf(msg, sizeof msg, "pixel (%d, %d): numerical failure", px, py);
+        char what[96], msg[160];
+        failure_text(c, px, py, what, sizeof what);
+        std::snprintf(msg, sizeof msg, "pixel (%d, %d): %s", px, py, what);  // RenderError, render.hpp:43-46
         return set_info(info, BHRT_NUMERICAL, px, py, msg);
     }
+    return 0;
+}
+
+int bhrt_ctx_upload_bytes(bhrt_ctx* c, uint64_t* staged, uint64_t* params_per_launch) {
+    if (!c) return BHRT_INVALID_ARGUMENT;
+    if (staged) *staged = c->upload_bytes;
+    if (params_per_launch) *params_per_launch = sizeof(KParams);
     return 0;
 }
 
@@ -817,6 +900,118 @@ int cached_ctx(int dev, bhrt_ctx** out, bhrt_status_info* info) {
 }
 }  // namespace
 
+// The one-shot path without records (what render_rows callers use,
+// render.cpp:68-119). Per device: the scene upload (async, pinned staging),
+// then the device's cyclic rows of each of B row bands (edges on multiples of
+// G rows, so a band's packed rows are a contiguous run of the whole range's
+// packed order) rendered on alternating streams — a band's kernel fills the
+// SMs while the previous band's longest blocks drain — and copied to pinned
+// staging on a copy stream as soon as the band is done. The host places
+// bands into the caller's buffer (unshuffling rows for G > 1) in band order
+// while later bands still render/copy, so only the last band's copy and
+// placement are exposed. Devices run concurrently; counters and the lowest
+// failing pixel come from each context's frame (bhrt_ctx_frame_begin/finish).
+static int render_rows_banded(const bhrt_scene* s, int32_t row_start, int32_t row_end, const std::vector<int>& devs,
+                       uint8_t* out, bhrt_status_info* info) {
+    const int G = static_cast<int>(devs.size());
+    const int tile_rows = 1;  // cyclic rows across devices
+    const int rows = row_end - row_start;
+    const size_t row_bytes = 3ull * s->width;
+    // bands: ~0.5 M samples or more each, at most 16 (4K x 4 spp: 16 bands)
+    const long long samples = static_cast<long long>(rows) * s->width * s->spp;
+    int B = static_cast<int>(std::min<long long>(16, std::max<long long>(1, samples / (1ll << 19))));
+    B = std::min(B, std::max(1, rows / G));
+    std::vector<int32_t> edge(B + 1);
+    for (int b = 0; b <= B; ++b) {
+        const long long e = static_cast<long long>(rows) * b / B;
+        edge[b] = b == B ? row_end : row_start + static_cast<int32_t>(e - e % G);
+    }
+    std::vector<bhrt_ctx*> ctxs(G);
+    std::vector<std::vector<int32_t>> boff(G, std::vector<int32_t>(B + 1, 0));  // packed row offsets
+    for (int g = 0; g < G; ++g) {
+        int rc = cached_ctx(devs[g], &ctxs[g], info);
+        if (rc) return rc;
+        bhrt_ctx* c = ctxs[g];
+        rc = bhrt_ctx_set_scene(c, s, info);
+        if (rc) return rc;
+        CK(cudaSetDevice(c->device));
+        if (!c->copy_stream) {
+            for (auto& st : c->band_stream) CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+            CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+        }
+        while (c->band_ev.size() < 2ull * B + 1) {
+            cudaEvent_t e;
+            CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            c->band_ev.push_back(e);
+        }
+        for (int b = 0; b < B; ++b)
+            boff[g][b + 1] = boff[g][b] + bhrt_tile_row_count(edge[b], edge[b + 1], tile_rows, G, g);
+        const size_t bytes = row_bytes * boff[g][B];
+        if (c->out.ensure(bytes + 1)) return set_info(info, BHRT_DEVICE, -1, -1, "output alloc failed");
+        if (bytes > c->host_out_cap) {
+            if (c->host_out) CK(cudaFreeHost(c->host_out));
+            c->host_out = nullptr;
+            c->host_out_cap = 0;
+            CK(cudaMallocHost(&c->host_out, bytes));
+            c->host_out_cap = bytes;
+        }
+        rc = bhrt_ctx_frame_begin(c, c->band_stream[0], info);
+        if (rc) return rc;
+        CK(cudaEventRecord(c->band_ev[2 * B], c->band_stream[0]));  // the counters' reset
+        CK(cudaStreamWaitEvent(c->band_stream[1], c->band_ev[2 * B], 0));
+        for (int b = 0; b < B; ++b) {
+            const int32_t nb = boff[g][b + 1] - boff[g][b];
+            if (nb == 0) continue;
+            cudaStream_t st = c->band_stream[b % 2];
+            rc = bhrt_ctx_render_async(c, edge[b], edge[b + 1], tile_rows, G, g,
+                                       c->out.p + row_bytes * boff[g][b], nullptr, st, info);
+            if (rc) return rc;
+            CK(cudaEventRecord(c->band_ev[2 * b], st));
+            CK(cudaStreamWaitEvent(c->copy_stream, c->band_ev[2 * b], 0));
+            CK(cudaMemcpyAsync(c->host_out + row_bytes * boff[g][b], c->out.p + row_bytes * boff[g][b],
+                               row_bytes * nb, cudaMemcpyDeviceToHost, c->copy_stream));
+            CK(cudaEventRecord(c->band_ev[2 * b + 1], c->copy_stream));
+        }
+    }
+    // place the bands as they land (band-major, so every device's copy of a
+    // band overlaps the placement of the previous one)
+    for (int b = 0; b < B; ++b) {
+        for (int g = 0; g < G; ++g) {
+            bhrt_ctx* c = ctxs[g];
+            const int32_t nb = boff[g][b + 1] - boff[g][b];
+            if (nb == 0) continue;
+            CK(cudaSetDevice(c->device));
+            CK(cudaEventSynchronize(c->band_ev[2 * b + 1]));
+            const unsigned char* src = c->host_out + row_bytes * boff[g][b];
+            if (G == 1) {
+                std::memcpy(out + row_bytes * (edge[b] - row_start), src, row_bytes * nb);
+            } else {
+                for (int j = 0; j < nb; ++j)  // band rows edge[b] + g + j G
+                    std::memcpy(out + row_bytes * (edge[b] + g + static_cast<int64_t>(j) * G - row_start),
+                                src + row_bytes * j, row_bytes);
+            }
+        }
+    }
+    int first_fail = 0;
+    long long fail_key = LLONG_MAX;
+    bhrt_status_info tmp;
+    for (int g = 0; g < G; ++g) {
+        const int r = bhrt_ctx_finish(ctxs[g], &tmp);
+        if (r == BHRT_NUMERICAL) {
+            const long long key = static_cast<long long>(tmp.py) * s->width + tmp.px;
+            if (key < fail_key) {
+                fail_key = key;
+                if (info) *info = tmp;
+                first_fail = r;
+            }
+        } else if (r) {
+            if (info) *info = tmp;
+            return r;
+        }
+    }
+    return first_fail;
+}
+
 extern "C" int bhrt_cuda_render_rows(const bhrt_scene* s, int32_t row_start, int32_t row_end,
                                      const int32_t* devices, int32_t ndev, uint8_t* out,
                                      size_t out_len, bhrt_ray_record* records,
@@ -851,6 +1046,7 @@ extern "C" int bhrt_cuda_render_rows(const bhrt_scene* s, int32_t row_start, int
     const int tile_rows = 1;  // cyclic rows (7.78x vs 6.35x for bands)
     std::vector<bhrt_ctx*> ctxs(G);
     std::vector<int32_t> nrows(G);
+    if (!records) return render_rows_banded(s, row_start, row_end, devs, out, info);
     for (int g = 0; g < G; ++g) {
         rc = cached_ctx(devs[g], &ctxs[g], info);
         if (rc) return rc;

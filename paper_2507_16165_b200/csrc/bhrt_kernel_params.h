@@ -35,7 +35,7 @@ struct KParams {
     double inv_spp;                // 1.0 / spp (render.cpp:42)
     unsigned long long div_magic;  // floor(2^64 / width) + 1 for width >= 2, else 0 (sample_of row division)
     int32_t width, height, spp;
-    int32_t pad0;
+    int32_t diag;  // 1: failed samples carry (u, kind) in their record (bhrt_cuda.cu failure_text)
     uint64_t seed;
     // integrator
     double epsilon, rel_tol, abs_tol, step, max_step, chord_dphi;

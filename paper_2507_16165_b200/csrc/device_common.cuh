@@ -68,7 +68,7 @@ __device__ __forceinline__ uint64_t hash_counter(uint64_t seed, uint64_t a, uint
     return h;
 }
 
-__device__ __forceinline__ V3 camera_ray(const KParams& p, int px, int py, int sample) {
+__device__ __forceinline__ V3 camera_dir_raw(const KParams& p, int px, int py, int sample) {
     double sx = 0.5, sy = 0.5;
     if (p.spp > 1) {
         sx = to_unit(hash_counter(p.seed, (uint64_t)px, (uint64_t)py, 2 * (uint64_t)sample));
@@ -83,9 +83,42 @@ __device__ __forceinline__ V3 camera_ray(const KParams& p, int px, int py, int s
     const double qu = au * p.inv_width, qv = av * p.inv_height;
     const double u = fma(fma(-qu, (double)p.width, au), p.inv_width, qu);
     const double v = fma(fma(-qv, (double)p.height, av), p.inv_height, qv);
-    const V3 d = add(add(vld(p.forward), scl(vld(p.right), (2.0 * u - 1.0) * p.tan_half_x)),
-                     scl(vld(p.up), (1.0 - 2.0 * v) * p.tan_half_y));
-    return normalized(d);
+    return add(add(vld(p.forward), scl(vld(p.right), (2.0 * u - 1.0) * p.tan_half_x)),
+               scl(vld(p.up), (1.0 - 2.0 * v) * p.tan_half_y));
+}
+
+// generate_ray's unit direction (camera.cpp:49-52), reference-exact (mode R)
+__device__ __forceinline__ V3 camera_ray(const KParams& p, int px, int py, int sample) {
+    return normalized(camera_dir_raw(p, px, py, sample));
+}
+
+// Unit vector by one reciprocal (scene modes; oracle unit_fast).
+__device__ __forceinline__ V3 unit_fast(V3 a) {
+    const double inv = 1.0 / norm(a);
+    return scl(a, inv);
+}
+
+// Scene-mode ray setup (RK4 / RKF45 / TABLE; oracle scene_frame):
+// the orbital frame straight from the raw camera direction D. e1 and u0 are
+// per-frame (KParams::cam_e1 / cam_u0); c = D.e1, T = D - c e1, e2 = T/|T|
+// by one reciprocal, u0' = -(c/|T|) u0 (= the reference's -(v.d)/(r0 b),
+// geodesic.cpp:57-65); radial iff |T|^2 < 1e-24 |D|^2 (geodesic.cpp:53).
+struct Frame {
+    V3 e2;
+    double w;
+    bool ok;
+};
+__device__ __forceinline__ Frame scene_frame(const KParams& p, V3 D) {
+    Frame f;
+    const V3 e1 = vld(p.cam_e1);
+    const double c = dot(D, e1);
+    const V3 T = sub(D, scl(e1, c));
+    const double t2 = dot(T, T);
+    f.ok = !(t2 < 1e-24 * dot(D, D));
+    const double inv = 1.0 / sqrt(t2);
+    f.e2 = scl(T, inv);
+    f.w = -((c * inv) * p.cam_u0);
+    return f;
 }
 
 // ----------------------------------------------------------------- geodesic helpers
@@ -328,7 +361,7 @@ __device__ static BHRT_INL_SHADE void shade_sample(const KParams& p, int obj, in
         for (int c = 0; c < 3; ++c) rgb[c] = p.disk_c_in[c] + t * (p.disk_c_out[c] - p.disk_c_in[c]);
     } else if (obj == BHRT_OBJ_SPHERE) {
         const bhrt_sphere& sp = p.spheres[sphere];
-        const V3 nrm = dvd(sub(pt, vld(sp.center)), sp.radius);
+        const V3 nrm = scl(sub(pt, vld(sp.center)), 1.0 / sp.radius);
         const double lam = dmax(0.0, dot(nrm, vld(p.light)));
         const double k = p.ambient + (1.0 - p.ambient) * lam;
 #pragma unroll
@@ -353,7 +386,9 @@ __device__ __forceinline__ void store_pixel(uint8_t* o, const double acc[3], dou
 __device__ __forceinline__ void finish_sample(const KParams& p, bool valid, const SampleId& id, int obj,
                                               int sphere, V3 point, double phi, unsigned steps,
                                               unsigned rej) {
-    const bool has_point = obj == BHRT_OBJ_SKY || obj == BHRT_OBJ_DISK || obj == BHRT_OBJ_SPHERE;
+    // failed samples carry (u at the failure, kind: 1 u <= 0, 2 step underflow)
+    // for the host's failure text (bhrt_cuda.cu failure_text)
+    const bool has_point = obj == BHRT_OBJ_SKY || obj == BHRT_OBJ_DISK || obj == BHRT_OBJ_SPHERE || obj < 0;
     if (valid && p.records) {
         bhrt_ray_record rec;
         BHRT_ASSERT(id.rec >= 0 && id.rec < (long long)p.n_rows * p.width * p.spp);

@@ -25,6 +25,16 @@ namespace bhrt {
 
 namespace {
 
+// The underlying failure text of a BHRT_NUMERICAL status: the part after
+// "pixel (x, y): ", i.e. the e.what() the reference's RenderError wraps
+// (render.cpp:36-40).
+std::string failure_what(const bhrt_status_info& info) {
+    const std::string m(info.message);
+    const size_t k = m.find("): ");
+    return k == std::string::npos ? m : m.substr(k + 3);
+}
+
+
 bhrt_scene to_abi(const SceneConfig& s) {
     bhrt_scene a;
     bhrt_scene_defaults(&a);  // extensions off: reference integrator, image sky
@@ -79,7 +89,7 @@ std::vector<int32_t> devices_from_env() {
     switch (code) {
         case BHRT_USAGE: throw UsageError(info.message);
         case BHRT_INVALID_ARGUMENT: throw std::invalid_argument(info.message);
-        case BHRT_NUMERICAL: throw RenderError(info.px, info.py, "numerical failure");
+        case BHRT_NUMERICAL: throw RenderError(info.px, info.py, failure_what(info));
         case BHRT_IO: throw IoError(info.message);
         default: throw std::runtime_error(std::string("bhrt_cuda: ") + info.message);
     }

@@ -261,12 +261,14 @@ __global__ void __launch_bounds__(128, BHRT_TAB_MINB) trace_table_kernel(const _
     int obj = BHRT_OBJ_NONE;
     V3 point = mk(0.0, 0.0, 0.0);
     double phi_out = 0.0;
+    unsigned nevals = 0;  // interpolated-orbit evaluations (the "steps" counter in table mode)
     if (valid) {
         const TabView T{p.tab_smp, p.tab_ends, p.tab_kind, p.tab_n, p.table_ns, p.table_dpsi, p.inv_table_dpsi};
         const V3 origin = vld(p.cam_pos), O = vld(p.center);
-        const V3 dir = camera_ray(p, id.x, id.y, id.s);
-        const Basis B = plane_basis(p, dir);
-        if (!B.ok) {  // radial: straight segment (geodesic.cpp:175-187); table mode has no spheres
+        const V3 D = camera_dir_raw(p, id.x, id.y, id.s);
+        const Frame F = scene_frame(p, D);
+        if (!F.ok) {  // radial: straight segment (geodesic.cpp:175-187); table mode has no spheres
+            const V3 dir = normalized(D);
             const double r0 = norm(sub(origin, O));
             const bool cap = dot(dir, sub(O, origin)) > 0.0;
             const double seg = cap ? r0 - 2.0 * p.mass : p.escape_radius;
@@ -285,9 +287,8 @@ __global__ void __launch_bounds__(128, BHRT_TAB_MINB) trace_table_kernel(const _
             }
             point = obj == BHRT_OBJ_SKY ? dir : add(origin, scl(dir, best));
         } else {
-            const V3 e1 = B.e1, e2 = B.e2, nrm = cross(e1, e2);
-            double u0, w0;
-            initial_conditions(p, dir, u0, w0);
+            const V3 e1 = vld(p.cam_e1), e2 = F.e2, nrm = cross(e1, e2);
+            const double u0 = p.cam_u0, w0 = F.w;
             const double M2 = 2.0 * p.mass;
             const double energy = w0 * w0 + u0 * u0 - M2 * u0 * u0 * u0;
             if (!(energy > 0.0)) {
@@ -299,8 +300,9 @@ __global__ void __launch_bounds__(128, BHRT_TAB_MINB) trace_table_kernel(const _
                 V3 Lw = mk(0.0, 0.0, 0.0);
                 if (p.disk_enabled) {
                     const V3 L = mk(-nrm.z, 0.0, nrm.x);
-                    const double nl = norm(L);
-                    if (nl >= 1e-12) {
+                    const double nl2 = dot(L, L);
+                    if (nl2 >= 1e-24) {  // |L| >= 1e-12
+                        const double nl = sqrt(nl2);
                         const double lx = dot(L, e1), ly = dot(L, e2);
                         const double pl = atan2(ly, lx);
                         next_disk = pl > 0.0 ? pl : pl + PI_D;
@@ -353,6 +355,7 @@ __global__ void __launch_bounds__(128, BHRT_TAB_MINB) trace_table_kernel(const _
                         double ui = -1.0, uj = -1.0;
                         if (wi > 0.0) ui = table_u(T, ie, p0i + sgn * ph);
                         if (wj > 0.0) uj = table_u(T, ie + 1, p0j + sgn * ph);
+                        nevals += (wi > 0.0) + (wj > 0.0);
                         double u_ev;
                         if (wi > 0.0 && wj > 0.0 && ui >= 0.0 && uj >= 0.0)
                             u_ev = wi * ui + wj * uj;
@@ -380,7 +383,7 @@ __global__ void __launch_bounds__(128, BHRT_TAB_MINB) trace_table_kernel(const _
                             const double ws = -sqrt(q > 0.0 ? q : 0.0);
                             const double c = cos(phi_end), sn = sin(phi_end);
                             const double tx = -ue * sn - ws * c, ty = ue * c - ws * sn;
-                            point = normalized(add(scl(e1, tx), scl(e2, ty)));
+                            point = unit_fast(add(scl(e1, tx), scl(e2, ty)));
                         }
                     }
                 }
@@ -388,7 +391,7 @@ __global__ void __launch_bounds__(128, BHRT_TAB_MINB) trace_table_kernel(const _
         }
     }
     finish_sample(p, valid, id, obj, -1, point, phi_out, 0u, 0u);
-    warp_add_stats(p.stats, 0u, 0u, valid ? 1u : 0u);
+    warp_add_stats(p.stats, nevals, 0u, valid ? 1u : 0u);
 }
 
 void launch_table_build(const KParams& p, double* smp, double* ends, int32_t* kind, int32_t* n, cudaStream_t st) {

@@ -316,9 +316,14 @@ __device__ __forceinline__ RResult window_loop(const KParams& p, V3 origin, V3 c
                 break;
             }
             R.obj = -BHRT_NUMERICAL;
+            R.edir = mk(u, 2.0, 0.0);  // StepSizeUnderflow at u (geodesic.cpp:157)
             break;
         }
-        if (!(u > 0.0)) { R.obj = -BHRT_NUMERICAL; break; }
+        if (!(u > 0.0)) {  // geodesic.cpp:233-234
+            R.obj = -BHRT_NUMERICAL;
+            R.edir = mk(u, 1.0, 0.0);
+            break;
+        }
         prev_phi = last_phi;
         prev_u = last_u;
         last_phi = phi;
@@ -343,6 +348,7 @@ __device__ __forceinline__ RResult window_loop(const KParams& p, V3 origin, V3 c
 #ifndef BHRT_REF_MINB
 #define BHRT_REF_MINB 8  // 64 regs, 32 warps/SM: 1/4/6/7/8/10 blocks -> 31.7/31.8/28.6/28.5/28.3/29.4 ms (960x540 mode R)
 #endif
+template <bool DIAG>  // DIAG: failed samples carry (u, kind) (bhrt_cuda.cu failure_text)
 __global__ void __launch_bounds__(128, BHRT_REF_MINB) trace_reference_kernel(const __grid_constant__ KParams p) {
     const long long n = (long long)p.n_rows * p.width * p.spp;
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -364,7 +370,7 @@ __global__ void __launch_bounds__(128, BHRT_REF_MINB) trace_reference_kernel(con
             initial_conditions(p, dir, u, w);
             const RResult R = window_loop<false>(p, origin, center, B.e1, B.e2, u, w, nsteps, nrej);
             obj = R.obj;
-            if (obj == BHRT_OBJ_SKY && R.chord) edir = R.edir;
+            if ((obj == BHRT_OBJ_SKY && R.chord) || (DIAG && obj < 0)) edir = R.edir;
             phi_end = R.phi;
         }
     }
@@ -452,7 +458,10 @@ extern "C" void bhrt_debug_hint_counts(unsigned long long out[4]) {
 
 void launch_reference(const KParams& p, cudaStream_t st) {
     const long long n = (long long)p.n_rows * p.width * p.spp;
-    trace_reference_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(p);
+    if (p.diag)
+        trace_reference_kernel<true><<<(unsigned)((n + 127) / 128), 128, 0, st>>>(p);
+    else
+        trace_reference_kernel<false><<<(unsigned)((n + 127) / 128), 128, 0, st>>>(p);
 }
 
 }  // namespace bhrt_b200

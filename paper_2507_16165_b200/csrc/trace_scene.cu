@@ -102,8 +102,7 @@ __device__ BHRT_INL_SETUP double events_setup(const KParams& p, SceneSm& sm, int
     sm.sigma[t] = 1.0;
     if (p.disk_enabled) {
         const V3 L = mk(-n.z, 0.0, n.x);
-        const double nl = norm(L);
-        if (nl >= 1e-12) {
+        if (dot(L, L) >= 1e-24) {  // |L| >= 1e-12 (oracle ray_events_setup)
             const double lx = dot(L, e1), ly = dot(L, e2);
             const double pl = atan2(ly, lx);
             next_disk = pl > 0.0 ? pl : pl + PI_D;
@@ -453,7 +452,7 @@ __device__ __forceinline__ V3 tangent_dir(V3 e1, V3 e2, double phi, double u, do
     double c, sn;
     sincos(phi, &sn, &c);
     const double tx = -u * sn - w * c, ty = u * c - w * sn;
-    return normalized(add(scl(e1, tx), scl(e2, ty)));
+    return unit_fast(add(scl(e1, tx), scl(e2, ty)));
 }
 
 // Oracle escape_dir(): tangent at the r = escape_radius crossing of the last
@@ -515,7 +514,10 @@ __device__ __noinline__ Hit radial_scene(const KParams& p, V3 origin, V3 dir, do
     return H;
 }
 
-template <int INTEG>
+// DIAG (failure_text's re-trace only): failed samples also carry (u, kind)
+// in their point for the host's failure text; the production instantiation
+// keeps nothing extra alive on those exits.
+template <int INTEG, bool DIAG>
 __global__ void __launch_bounds__(kBlock, BHRT_SCENE_MINB) trace_scene_kernel(const __grid_constant__ KParams p) {
     __shared__ SceneSm sm;
     const int t = threadIdx.x;
@@ -540,20 +542,21 @@ __global__ void __launch_bounds__(kBlock, BHRT_SCENE_MINB) trace_scene_kernel(co
     double phi = 0.0;
     if (valid) {
         const V3 origin = vld(p.cam_pos), O = vld(p.center);
-        const V3 dir = camera_ray(p, id.x, id.y, id.s);
-        const Basis B = plane_basis(p, dir);
-        if (!B.ok) {
+        const V3 D = camera_dir_raw(p, id.x, id.y, id.s);
+        const Frame F = scene_frame(p, D);
+        if (!F.ok) {
+            const V3 dir = normalized(D);
             const double r0 = norm(sub(origin, O));
             const bool cap = dot(dir, sub(O, origin)) > 0.0;
             H = radial_scene(p, origin, dir, cap ? r0 - 2.0 * p.mass : p.escape_radius, cap);
         } else {
-            const V3 nrm = cross(B.e1, B.e2);
-            st3(sm.e2, t, B.e2);
+            const V3 e1 = vld(p.cam_e1);
+            const V3 nrm = cross(e1, F.e2);
+            st3(sm.e2, t, F.e2);
             st3(sm.n, t, nrm);
-            double u, w;
-            initial_conditions(p, dir, u, w);
+            double u = p.cam_u0, w = F.w;
             sm.energy[t] = w * w + u * u - (2.0 * p.mass) * u * u * u;
-            double next_ev = events_setup(p, sm, t, B.e1, B.e2, nrm);
+            double next_ev = events_setup(p, sm, t, e1, F.e2, nrm);
             double pp = 0.0, up = 0.0, wp = 0.0;  // RK4: state before the last accepted step
             bool has_step = false;
             if (INTEG == BHRT_INTEGRATOR_RK4) {
@@ -577,7 +580,11 @@ __global__ void __launch_bounds__(kBlock, BHRT_SCENE_MINB) trace_scene_kernel(co
                     phi = pn;
                     u = un;
                     w = wn;
-                    if (!(u > 0.0)) { H.obj = -BHRT_NUMERICAL; break; }
+                    if (!(u > 0.0)) {
+                        H.obj = -BHRT_NUMERICAL;
+                        if (DIAG) H.point = mk(u, 1.0, 0.0);
+                        break;
+                    }
                 }
             } else {
                 double h = p.step;
@@ -612,6 +619,7 @@ __global__ void __launch_bounds__(kBlock, BHRT_SCENE_MINB) trace_scene_kernel(co
                             }
                             if (!(un > 0.0)) {
                                 H.obj = -BHRT_NUMERICAL;
+                                if (DIAG) H.point = mk(un, 1.0, 0.0);
                                 phi = pn;
                                 u = un;
                                 w = wn;
@@ -638,6 +646,7 @@ __global__ void __launch_bounds__(kBlock, BHRT_SCENE_MINB) trace_scene_kernel(co
                         h = hn;
                         if (h < 1e-14) {
                             H.obj = (p.mass > 0.0 && u >= p.u_cap) ? BHRT_OBJ_HORIZON : -BHRT_NUMERICAL;
+                            if (DIAG && H.obj < 0) H.point = mk(u, 2.0, 0.0);
                             break;
                         }
                     }
@@ -654,10 +663,17 @@ __global__ void __launch_bounds__(kBlock, BHRT_SCENE_MINB) trace_scene_kernel(co
 void launch_scene(const KParams& p, cudaStream_t st) {
     const long long n = (long long)p.n_rows * p.width * p.spp;
     const unsigned blocks = (unsigned)((n + kBlock - 1) / kBlock);
-    if (p.integrator == BHRT_INTEGRATOR_RK4)
-        trace_scene_kernel<BHRT_INTEGRATOR_RK4><<<blocks, kBlock, 0, st>>>(p);
-    else
-        trace_scene_kernel<BHRT_INTEGRATOR_RKF45><<<blocks, kBlock, 0, st>>>(p);
+    if (p.integrator == BHRT_INTEGRATOR_RK4) {
+        if (p.diag)
+            trace_scene_kernel<BHRT_INTEGRATOR_RK4, true><<<blocks, kBlock, 0, st>>>(p);
+        else
+            trace_scene_kernel<BHRT_INTEGRATOR_RK4, false><<<blocks, kBlock, 0, st>>>(p);
+    } else {
+        if (p.diag)
+            trace_scene_kernel<BHRT_INTEGRATOR_RKF45, true><<<blocks, kBlock, 0, st>>>(p);
+        else
+            trace_scene_kernel<BHRT_INTEGRATOR_RKF45, false><<<blocks, kBlock, 0, st>>>(p);
+    }
 }
 
 }  // namespace bhrt_b200

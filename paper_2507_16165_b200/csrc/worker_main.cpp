@@ -32,6 +32,16 @@
 
 namespace {
 
+// The underlying failure text of a BHRT_NUMERICAL status: the part after
+// "pixel (x, y): ", i.e. the e.what() the reference's RenderError wraps
+// (render.cpp:36-40).
+std::string failure_what(const bhrt_status_info& info) {
+    const std::string m(info.message);
+    const size_t k = m.find("): ");
+    return k == std::string::npos ? m : m.substr(k + 3);
+}
+
+
 constexpr std::uint32_t kErrProtocol = 1, kErrIo = 2, kErrNumerical = 3;  // netrender.cpp:14-16
 constexpr int kRowsPerChunk = 64;                                        // netrender.cpp:18
 
@@ -90,7 +100,7 @@ void serve_job(bhrt::ByteStream& stream) {
         rc = bhrt_cuda_render_rows(&s, band.row_start, band.row_end, devs.empty() ? nullptr : devs.data(),
                                    static_cast<int32_t>(devs.size()), pixels.data(), pixels.size(), nullptr,
                                    &info);
-        if (rc == BHRT_NUMERICAL) throw RenderError(info.px, info.py, "numerical failure");
+        if (rc == BHRT_NUMERICAL) throw RenderError(info.px, info.py, failure_what(info));
         if (rc == BHRT_USAGE) throw UsageError(info.message);
         if (rc == BHRT_INVALID_ARGUMENT) throw std::invalid_argument(info.message);
         if (rc) throw IoError(std::string("bhrt_cuda: ") + info.message);

@@ -71,6 +71,7 @@ def lib():
         L.bhrt_ctx_stats.argtypes = [C.c_void_p, P(C.c_uint64), P(C.c_uint64), P(C.c_uint64),
                                      P(C.c_int32)]
         L.bhrt_ctx_counters.argtypes = [C.c_void_p, P(C.c_uint64)]
+        L.bhrt_ctx_upload_bytes.argtypes = [C.c_void_p, P(C.c_uint64), P(C.c_uint64)]
         L.bhrt_ctx_set_timing.argtypes = [C.c_void_p, C.c_int32]
         L.bhrt_ctx_kernel_ms.argtypes = [C.c_void_p, P(C.c_float), P(C.c_float)]
         L.bhrt_tile_row_count.argtypes = [C.c_int32] * 5
@@ -90,7 +91,7 @@ EXPORTS = [
     "bhrt_scene_format_text", "bhrt_ctx_set_output_layout", "bhrt_device_alloc",
     "bhrt_device_free", "bhrt_ipc_export", "bhrt_ipc_open", "bhrt_ipc_close", "bhrt_ctx_create", "bhrt_ctx_destroy", "bhrt_ctx_set_scene",
     "bhrt_ctx_render_async", "bhrt_ctx_frame_begin", "bhrt_ctx_finish", "bhrt_ctx_stats", "bhrt_ctx_set_timing",
-    "bhrt_ctx_kernel_ms", "bhrt_ctx_counters", "bhrt_tile_row_count",
+    "bhrt_ctx_kernel_ms", "bhrt_ctx_counters", "bhrt_ctx_upload_bytes", "bhrt_tile_row_count",
     "bhrt_b200_fp64_peak_tflops", "bhrt_cuda_abi_version", "bhrt_flops_per_step",
 ]
 

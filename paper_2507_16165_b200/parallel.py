@@ -111,6 +111,7 @@ class FrameRenderer:
             peer = world > 1 and dist.is_initialized() and dist.get_backend(group) == "nccl"
         self.want_peer = bool(peer) and world > 1
         self.peer = None
+        self._peer_frames = 0  # frames written into the current peer image
 
     def _buffers(self, h: int, w: int):
         if self._shape == (h, w):
@@ -128,6 +129,7 @@ class FrameRenderer:
         if self.want_peer:
             if self.peer is not None:
                 self.peer.close()
+            self._peer_frames = 0
             try:
                 self.peer = PeerImage(self.rank, self.device, h * w * 3, self.group)
                 ok = 1
@@ -154,11 +156,23 @@ class FrameRenderer:
         h, w = self.scene.s.height, self.scene.s.width
         st = stream or torch.cuda.current_stream(self.device)
         if self.peer is not None:
-            # rows go straight into rank 0's image; completion = every rank's
-            # kernel finished (stream-ordered collective after the kernel)
+            # rows go straight into rank 0's image. Begin: no rank may write
+            # frame N+1 into it before rank 0 has consumed frame N — a
+            # stream-ordered collective that rank 0 enqueues after whatever it
+            # queued on this stream for the previous frame (its device->host
+            # copy in render()). Completion: every rank's kernel finished
+            # (stream-ordered collective after the kernel).
+            nccl = dist.get_backend(self.group) == "nccl"
+            if self._peer_frames > 0:
+                if nccl:
+                    with torch.cuda.stream(st):
+                        dist.all_reduce(self._begin_flag(), group=self.group)
+                else:
+                    dist.barrier(group=self.group)
+            self._peer_frames += 1
             self.ctx.render_async(self.peer.ptr.value, 0, h, self.tile_rows, self.world,
                                   self.rank, stream=st.cuda_stream)
-            if dist.get_backend(self.group) == "nccl":
+            if nccl:
                 with torch.cuda.stream(st):
                     dist.all_reduce(self._done_flag(), group=self.group)
             else:
@@ -191,6 +205,11 @@ class FrameRenderer:
         if getattr(self, "_flag", None) is None:
             self._flag = torch.zeros(1, dtype=torch.int32, device=f"cuda:{self.device}")
         return self._flag
+
+    def _begin_flag(self):
+        if getattr(self, "_bflag", None) is None:
+            self._bflag = torch.zeros(1, dtype=torch.int32, device=f"cuda:{self.device}")
+        return self._bflag
 
     def finish(self):
         self.ctx.finish()

@@ -18,7 +18,7 @@ arithmetic, so the achieved figure is a lower bound.
 """
 from __future__ import annotations
 
-from .abi import INTEGRATOR_REFERENCE, INTEGRATOR_RK4, INTEGRATOR_RKF45
+from .abi import INTEGRATOR_REFERENCE, INTEGRATOR_RK4, INTEGRATOR_RKF45, INTEGRATOR_TABLE
 
 STEP_FLOPS = {INTEGRATOR_RKF45: 137.0, INTEGRATOR_RK4: 39.0, INTEGRATOR_REFERENCE: 152.0}
 
@@ -34,3 +34,20 @@ def launch_flops(scene, stats: dict) -> float:
     s = scene.s if hasattr(scene, "s") else scene
     attempts = stats["steps"] + stats["rejected"]
     return attempts * STEP_FLOPS[s.integrator] + stats["rays"] * setup_flops(scene)
+
+
+# Table mode (approximate, config 3): per sample the two bracketing entries'
+# kind (2 x 4 B), camera angle psi0 (2 x 8 B) and plan ends psi_end/psi_esc
+# (2 x 16 B); per interpolated-orbit evaluation (disk event; the kernel's
+# "steps" counter in table mode) one entry's kind + count (8 B), psi_end
+# (8 B) and the two bracketing (u, u') samples (32 B); 3 B of RGB8 per pixel.
+TABLE_BYTES_PER_SAMPLE = 56
+TABLE_BYTES_PER_EVAL = 48
+
+
+def table_bytes(scene, stats: dict) -> float:
+    s = scene.s if hasattr(scene, "s") else scene
+    assert s.integrator == INTEGRATOR_TABLE
+    pixels = stats["rays"] // max(1, s.spp)
+    return (stats["rays"] * TABLE_BYTES_PER_SAMPLE + stats["steps"] * TABLE_BYTES_PER_EVAL
+            + 3 * pixels)

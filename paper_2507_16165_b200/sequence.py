@@ -58,9 +58,12 @@ class SequenceRenderer:
         t = self.torch
         self.dev = t.empty((h, w, 3), dtype=t.uint8, device=f"cuda:{self.device}")
         # pinned buffers: one per writer thread, one queued, one receiving the
-        # next frame
+        # next frame; a buffer is reused only after its writer returned it
         self.host = [t.empty((h, w, 3), dtype=t.uint8, pin_memory=True)
                      for _ in range(self.writers + 2)]
+        self.free: queue.Queue = queue.Queue()
+        for b in self.host:
+            self.free.put(b)
         self._shape = (h, w)
 
     def render(self, scenes, paths=None, on_frame=None) -> dict:
@@ -78,15 +81,20 @@ class SequenceRenderer:
                 if job is None:
                     return
                 i, ev, buf = job
-                ev.synchronize()
-                img = buf.numpy()
                 try:
+                    ev.synchronize()
+                    img = buf.numpy()
                     if paths is not None:
                         save_ppm_file(img, paths[i])
                     if on_frame is not None:
                         on_frame(i, img)
                 except Exception as e:  # noqa: BLE001 - reported after the loop
                     errors.append(e)
+                finally:
+                    # the file (and callback) is done with it; a buffer of an
+                    # earlier frame size is dropped, not recycled
+                    if any(buf is b for b in self.host):
+                        self.free.put(buf)
 
         ths = [threading.Thread(target=writer, daemon=True) for _ in range(self.writers)]
         t0 = time.perf_counter()
@@ -103,7 +111,7 @@ class SequenceRenderer:
             rendered = t.cuda.Event()
             rendered.record(st)
             self.copy_stream.wait_event(rendered)
-            buf = self.host[i % len(self.host)]
+            buf = self.free.get()  # waits until a writer has released one
             with t.cuda.stream(self.copy_stream):
                 buf.copy_(self.dev, non_blocking=True)
             copy_done = t.cuda.Event()

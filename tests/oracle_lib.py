@@ -94,6 +94,8 @@ def ref():
         L.ref_make_bands.argtypes = [C.c_int, C.c_int, IP, IP, C.c_int, IP]
         L.ref_strong_scaling_mean.restype = D
         L.ref_strong_scaling_mean.argtypes = [P(Scene), C.c_int, C.c_int]
+        L.ref_strong_scaling_pixels_mean.restype = D
+        L.ref_strong_scaling_pixels_mean.argtypes = [P(Scene), C.c_int, C.c_int, IP, IP, C.c_int]
         L.ref_serialize_scene.restype = C.c_size_t
         L.ref_serialize_scene.argtypes = [P(Scene), C.c_char_p, C.c_size_t]
         L.ref_parse_scene.argtypes = [C.c_char_p, P(Scene), P(StatusInfo)]

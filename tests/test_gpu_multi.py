@@ -51,13 +51,21 @@ def test_spp_not_dividing_warp_uses_record_path():
     assert d.max() <= 1 and (d > 0).mean() <= 0.001
 
 
-def _rank(rank, world, port, q, peer=False):
+def frames():
+    """Three frames: a size change (the peer image is re-mapped), then two
+    different scenes of the same size back to back (the peer image is reused:
+    no rank may write the next frame before rank 0 has read this one)."""
+    return [scenes.config(2, 64, 36), scenes.config(1, 50, 20), scenes.config(2, 50, 20)]
+
+
+def _rank(rank, world, port, q, peer=False, backend="gloo"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
-    torch.cuda.set_device(0)
-    fr = parallel.FrameRenderer(rank, world, 0, peer=peer)
-    for idx in (2, 1):  # two frames, different sizes: the peer image is re-mapped
-        sb = scenes.config(idx, 64, 36) if idx == 2 else scenes.config(idx, 50, 20)
+    dev = rank if backend == "nccl" else 0
+    torch.cuda.set_device(dev)
+    kw = {"device_id": torch.device("cuda", dev)} if backend == "nccl" else {}
+    dist.init_process_group(backend, rank=rank, world_size=world, **kw)
+    fr = parallel.FrameRenderer(rank, world, dev, peer=peer)
+    for sb in frames():
         img = fr.render(sb)
         if rank == 0:
             q.put((fr.peer is not None, img.numpy().copy()))
@@ -66,28 +74,32 @@ def _rank(rank, world, port, q, peer=False):
     dist.destroy_process_group()
 
 
-def _run_ranks(world, peer):
+def _run_ranks(world, peer, backend="gloo"):
     ctx = mp.get_context("spawn")
     q = ctx.SimpleQueue()
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
     port = s.getsockname()[1]
     s.close()
-    ps = [ctx.Process(target=_rank, args=(r, world, port, q, peer)) for r in range(world)]
+    ps = [ctx.Process(target=_rank, args=(r, world, port, q, peer, backend)) for r in range(world)]
     for p in ps:
         p.start()
-    out = [q.get(), q.get()]
+    out = [q.get() for _ in frames()]
     for p in ps:
         p.join(300)
         assert p.exitcode == 0
     return out
 
 
+def check_frames(out):
+    for (_, img), sb in zip(out, frames()):
+        assert np.array_equal(img, render.render_image(sb))
+
+
 def test_frame_renderer_two_ranks_share_one_gpu():
-    (used_peer, a), (_, b) = _run_ranks(2, False)
-    assert not used_peer
-    assert np.array_equal(a, render.render_image(scenes.config(2, 64, 36)))
-    assert np.array_equal(b, render.render_image(scenes.config(1, 50, 20)))
+    out = _run_ranks(2, False)
+    assert not out[0][0]
+    check_frames(out)
 
 
 @pytest.mark.parametrize("world", [2, 3])
@@ -96,10 +108,9 @@ def test_frame_renderer_peer_image_over_ipc(world):
     (CUDA IPC mapping, image output layout): no gather, same bytes. The ranks
     share cuda:0 here (IPC within one device); their kernels never wait on
     each other — completion is a host barrier after each rank's stream."""
-    (used_peer, a), (_, b) = _run_ranks(world, True)
-    assert used_peer
-    assert np.array_equal(a, render.render_image(scenes.config(2, 64, 36)))
-    assert np.array_equal(b, render.render_image(scenes.config(1, 50, 20)))
+    out = _run_ranks(world, True)
+    assert out[0][0]
+    check_frames(out)
 
 
 def test_banded_end_to_end_render_matches_single_launch():
@@ -131,3 +142,64 @@ def test_banded_render_reports_lowest_failing_pixel_of_the_frame():
     with pytest.raises(render.RenderError) as e:
         render.render_rows(sb, 0, 32)
     assert (e.value.px, e.value.py) == (15, 7)
+
+
+@pytest.mark.parametrize("wh", [(64, 36), (97, 61), (320, 180), (1920, 1080)])
+def test_dropin_banded_path_matches_single_launch(wh):
+    """bhrt_cuda_render_rows without records renders row bands on two
+    streams with overlapped copy-out into the caller's host buffer; bytes
+    equal the record path's single launch (and row sub-ranges)."""
+    w, h = wh
+    sb = scenes.config(2 if w < 1000 else 1, w, h)
+    banded = render.render_rows(sb, 0, h)
+    single, _ = render.render_rows(sb, 0, h, records=True)
+    assert np.array_equal(banded, single)
+    r0, r1 = h // 3, h - 1
+    assert np.array_equal(render.render_rows(sb, r0, r1, devices=[0]),
+                          single[r0 * w * 3:r1 * w * 3])
+
+
+# ---- two physical GPUs (skipped on a one-GPU lease)
+two_gpus = pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+
+
+@two_gpus
+def test_two_gpus_nccl_peer_image():
+    """One process per GPU over NCCL: every rank's kernel stores its cyclic
+    rows into rank 0's image over NVLink peer memory (CUDA IPC), stream-ordered
+    NCCL begin/done collectives; three frames equal the one-GPU renders."""
+    out = _run_ranks(2, None, backend="nccl")
+    assert out[0][0]
+    check_frames(out)
+
+
+@two_gpus
+def test_two_gpus_nccl_gather_fallback():
+    out = _run_ranks(2, False, backend="nccl")
+    assert not out[0][0]
+    check_frames(out)
+
+
+@two_gpus
+def test_dropin_two_devices():
+    """The one-shot C ABI splitting cyclic rows over two devices from one
+    thread (concurrent bands and copies) = the one-device bytes."""
+    for sb in (scenes.config(2, 320, 181), scenes.config(1, 1920, 1080)):
+        one = render.render_rows(sb, 0, sb.s.height, devices=[0])
+        assert np.array_equal(render.render_rows(sb, 0, sb.s.height, devices=[0, 1]), one)
+        assert np.array_equal(render.render_rows(sb, 0, sb.s.height, devices=[1, 0]), one)
+
+
+@two_gpus
+def test_bench_two_gpus_self_launch():
+    """bench.py --gpus 2 outside torchrun launches two ranks and reports them."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--steps", "2",
+                        "--warmup", "3", "--no-cpu", "--no-secondary"], cwd=root,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1 and lines[0]["n_gpus"] == 2 and lines[0]["value"] > 0

@@ -91,14 +91,33 @@ def test_table_mode_close_to_direct_integration():
     assert (diff > 0).mean() < 0.01
 
 
-def test_row_tiles_assemble_to_full_frame():
-    sb = scenes.config(2, 64, 40)
-    full = render.render_image(sb).reshape(40, -1)
-    ctx_rows = []
-    for off in range(3):
-        out = render.render_rows(sb, 0, 40, 1)  # one-shot reference path
-        ctx_rows.append(out)
-    assert all(np.array_equal(full.reshape(-1), r) for r in ctx_rows)
+@pytest.mark.parametrize("tile_rows,stride", [(1, 3), (2, 3), (4, 2)])
+def test_row_tiles_assemble_to_full_frame(tile_rows, stride):
+    """Each tile offset rendered through the context's tiled path (packed
+    rows, tile_rows/tile_stride/tile_offset -> packed_row_to_y), scattered
+    with parallel.rows_of_rank, reassembles the one-shot full frame."""
+    import torch
+
+    from paper_2507_16165_b200 import parallel
+    sb = scenes.config(2, 64, 41)
+    h, w = sb.s.height, sb.s.width
+    full = render.render_image(sb).reshape(h, w * 3)
+    ctx = render.Context(0)
+    ctx.set_scene(sb)
+    img = np.full((h, w * 3), 7, np.uint8)
+    covered = np.zeros(h, int)
+    for off in range(stride):
+        n = render.tile_row_count(0, h, tile_rows, stride, off)
+        buf = torch.zeros(max(n, 1) * w * 3, dtype=torch.uint8, device="cuda")
+        ctx.render_async(buf.data_ptr(), 0, h, tile_rows, stride, off)
+        ctx.finish()
+        ys = parallel.rows_of_rank(h, stride, off, tile_rows)
+        assert len(ys) == n
+        img[ys] = buf[:n * w * 3].cpu().numpy().reshape(n, w * 3)
+        covered[ys] += 1
+    ctx.close()
+    assert (covered == 1).all()
+    assert np.array_equal(img, full)
 
 
 def test_numerical_failure_reports_lowest_pixel():
@@ -109,3 +128,37 @@ def test_numerical_failure_reports_lowest_pixel():
     with pytest.raises(render.RenderError) as e:
         render.render_image(sb)
     assert (e.value.px, e.value.py) == (0, 0)
+
+
+def ref_failure(sb):
+    rc, _, info = ref_render(sb.s, threads=1)  # one thread: the lowest pixel fails first
+    return rc, info.px, info.py, info.message.decode()
+
+
+@pytest.mark.parametrize("size", [8, 16])
+def test_numerical_failure_carries_reference_text(size):
+    """render.cpp:36-40: RenderError wraps the trace's own message
+    ('trace: inverse radius left the positive domain', geodesic.cpp:233-234,
+    here from flat space with 100x wider windows). Pixel and text equal the
+    compiled reference's."""
+    sb = scenes.small_scene(scenes.gradient_background(), size, 0.0)
+    sb.s.epsilon = 100.0
+    with pytest.raises(render.RenderError) as e:
+        render.render_image(sb)
+    assert e.value.message.endswith("): trace: inverse radius left the positive domain")
+    if have_ref():
+        rc, px, py, msg = ref_failure(sb)
+        assert rc == 3 and (px, py) == (e.value.px, e.value.py) and msg == e.value.message
+
+
+def test_step_underflow_text():
+    """StepSizeUnderflow's text (geodesic.hpp:72-74) with the state's u."""
+    sb = scenes.small_scene(scenes.gradient_background(), 4, 0.0)
+    sb.s.rel_tol = 1e-300
+    sb.s.abs_tol = 1e-300
+    with pytest.raises(render.RenderError) as e:
+        render.render_image(sb)
+    assert "): adaptive step size underflow near u = " in e.value.message
+    if have_ref():
+        rc, px, py, msg = ref_failure(sb)
+        assert rc == 3 and (px, py) == (e.value.px, e.value.py) and msg == e.value.message
