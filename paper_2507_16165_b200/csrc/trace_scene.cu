@@ -30,19 +30,26 @@ constexpr float kWinMargin = 5e-4f;  // fp32 window slack (rad); windows only cu
 #define BHRT_SCENE_MINB 5
 #endif
 
-struct SceneSm {
+// Per-ray slots (lane-major: slot index = ray's position in the block, so
+// a warp's 32 accesses hit 32 consecutive words — conflict-free).
+template <int NS>
+struct SceneSmT {
+    static constexpr int kNS = NS;
     float4 sph[kSphSm];  // (cx, cy, cz, r + fp32 slack) relative to the hole: cull prefilter
-    double e2[3][kBlock], n[3][kBlock];  // e1 is the per-frame KParams::cam_e1
-    double sigma[kBlock], energy[kBlock], next_disk[kBlock];
-    float lo[kSlots][kBlock], hi[kSlots][kBlock];   // angular window (unwrapped phi)
-    float rlo[kSlots][kBlock], rhi[kSlots][kBlock]; // radial extent of the circle
-    unsigned char k[kSlots][kBlock];
-    int nc[kBlock];
-    float next_sph[kBlock];
+    double e2[3][NS], n[3][NS];  // e1 is the per-frame KParams::cam_e1
+    double sigma[NS], energy[NS], next_disk[NS];
+    float lo[kSlots][NS], hi[kSlots][NS];   // angular window (unwrapped phi)
+    float rlo[kSlots][NS], rhi[kSlots][NS]; // radial extent of the circle
+    unsigned char k[kSlots][NS];
+    int nc[NS];
+    float next_sph[NS];
 };
+using SceneSm = SceneSmT<kBlock>;
 
-__device__ __forceinline__ V3 ld3(const double (&a)[3][kBlock], int t) { return {a[0][t], a[1][t], a[2][t]}; }
-__device__ __forceinline__ void st3(double (&a)[3][kBlock], int t, V3 v) {
+template <int NS>
+__device__ __forceinline__ V3 ld3(const double (&a)[3][NS], int t) { return {a[0][t], a[1][t], a[2][t]}; }
+template <int NS>
+__device__ __forceinline__ void st3(double (&a)[3][NS], int t, V3 v) {
     a[0][t] = v.x;
     a[1][t] = v.y;
     a[2][t] = v.z;
@@ -97,7 +104,8 @@ __device__ __forceinline__ void sphere_window_f(double cx, double cy, double rho
 
 // Disk line + sphere candidates (oracle ray_events_setup). Returns the first
 // event angle.
-__device__ BHRT_INL_SETUP double events_setup(const KParams& p, SceneSm& sm, int t, V3 e1, V3 e2, V3 n) {
+template <class SM>
+__device__ BHRT_INL_SETUP double events_setup(const KParams& p, SM& sm, int t, V3 e1, V3 e2, V3 n) {
     double next_disk = CUDART_INF;
     sm.sigma[t] = 1.0;
     if (p.disk_enabled) {
@@ -192,7 +200,8 @@ struct Hit {
 
 // Unit disk line in plane coordinates and world space (oracle ray_events_setup
 // values, same operations), formed only when a disk crossing lands in the annulus.
-__device__ __forceinline__ void disk_line(const KParams& p, const SceneSm& sm, int t, double& dlx, double& dly, V3& Lw) {
+template <class SM>
+__device__ __forceinline__ void disk_line(const KParams& p, const SM& sm, int t, double& dlx, double& dly, V3& Lw) {
     const V3 n = ld3(sm.n, t), e1 = vld(p.cam_e1), e2 = ld3(sm.e2, t);
     const V3 L = mk(-n.z, 0.0, n.x);
     const double nl = norm(L);
@@ -206,7 +215,8 @@ __device__ __forceinline__ void disk_line(const KParams& p, const SceneSm& sm, i
 // candidate slots overflowed). Rare after radial culling (~0.04 per ray on
 // config 2), so it is kept out of line: its registers do not count against
 // the step loop's occupancy.
-__device__ BHRT_INL_SPH bool sphere_search(const KParams& p, const SceneSm& sm, int t, double pa, double h,
+template <class SM>
+__device__ BHRT_INL_SPH bool sphere_search(const KParams& p, const SM& sm, int t, double pa, double h,
                                            double ua, double ub, const Cubic cu, unsigned act, int nc,
                                            int& bsph, double& bqx, double& bqy) {
     const bool test_all = nc < 0;
@@ -305,7 +315,8 @@ __device__ BHRT_INL_SPH bool sphere_search(const KParams& p, const SceneSm& sm, 
 // Oracle step_events(): disk = exact phi-event on the step's Hermite
 // interpolant; spheres = first entering hit on S equal-angle sub-chords.
 // Returns true on hit; always advances the event state and next_ev.
-__device__ BHRT_INL_EVT bool step_events(const KParams& p, SceneSm& sm, int t, double pa, double ua,
+template <class SM>
+__device__ BHRT_INL_EVT bool step_events(const KParams& p, SM& sm, int t, double pa, double ua,
                                          double wa, double pb, double ub, double wb, double& next_ev,
                                          Hit& hit) {
     const double h = pb - pa;
@@ -457,7 +468,8 @@ __device__ __forceinline__ V3 tangent_dir(V3 e1, V3 e2, double phi, double u, do
 
 // Oracle escape_dir(): tangent at the r = escape_radius crossing of the last
 // step (Hermite + 2 Newton iterations, u' from the first integral).
-__device__ BHRT_INL_ESC V3 escape_dir(const KParams& p, SceneSm& sm, int t, bool has_step, double pa,
+template <class SM>
+__device__ BHRT_INL_ESC V3 escape_dir(const KParams& p, SM& sm, int t, bool has_step, double pa,
                                       double ua, double wa, double pb, double ub, double wb) {
     const V3 e1 = vld(p.cam_e1), e2 = ld3(sm.e2, t);
     if (!has_step || !(ua > p.u_esc)) return tangent_dir(e1, e2, pb, ub, wb);
