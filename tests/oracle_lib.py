@@ -149,6 +149,19 @@ def orc_render(scene, rows=None, threads=8, records=False):
     return rc, out, info, recs
 
 
+def orc_render_np(scene, rows=None, threads=None):
+    """orc_render with the records as a numpy structured array (abi.record_dtype)."""
+    from paper_2507_16165_b200.abi import record_dtype
+    L = oracle()
+    r0, r1 = rows if rows else (0, scene.height)
+    out = np.zeros(((r1 - r0) * scene.width * 3,), np.uint8)
+    rec = np.zeros((r1 - r0) * scene.width * scene.spp, record_dtype())
+    info = StatusInfo()
+    rc = L.orc_render_rows(C.byref(scene), r0, r1, threads or os.cpu_count() or 1, u8p(out),
+                           rec.ctypes.data_as(C.POINTER(RayRecord)), C.byref(info))
+    return rc, out, info, rec
+
+
 def ref_render(scene, rows=None, threads=8):
     L = ref()
     r0, r1 = rows if rows else (0, scene.height)
