@@ -22,7 +22,7 @@ namespace bhrt_b200 {
 
 int launch_trace(const KParams& p, cudaStream_t st, int* launches, cudaEvent_t* ev);
 void launch_table_build(const KParams& p, double* smp, double* ends, int32_t* kind, int32_t* n, cudaStream_t st);
-void launch_table_bind(const KParams& p, double* ends, double* psi0, double u0, cudaStream_t st);
+void launch_table_bind(const KParams& p, double* ends, double* psi0, void* meta, double u0, cudaStream_t st);
 void launch_trace_polylines(const KParams& p, const double* rays, long long n, bhrt_ray_record* records,
                             double* pts, int cap, int* npoly, cudaStream_t st);
 void launch_trace_rays(const KParams& p, const double* rays, long long n, bhrt_ray_record* records,
@@ -214,8 +214,10 @@ struct bhrt_ctx {
     DevBuf<uint8_t> out;
     DevBuf<unsigned long long> stats;
     DevBuf<unsigned long long> cull;
+    DevBuf<float> sph_frame;  // KParams::sph_frame
     DevBuf<double> tab_smp, tab_ends, tab_psi0;
     DevBuf<int32_t> tab_kind, tab_n;
+    DevBuf<double> tab_meta;  // 6 doubles (48 B) per entry: table.cu TabMeta
     bool has_table = false;
     double table_key[10] = {0};
     cudaStream_t last_stream = nullptr;
@@ -444,6 +446,7 @@ void bhrt_ctx_destroy(bhrt_ctx* c) {
     c->out.release();
     c->stats.release();
     c->cull.release();
+    c->sph_frame.release();
     c->checker.release();
     c->rays.release();
     c->defl.release();
@@ -465,6 +468,7 @@ void bhrt_ctx_destroy(bhrt_ctx* c) {
     c->tab_psi0.release();
     c->tab_kind.release();
     c->tab_n.release();
+    c->tab_meta.release();
     delete c;
 }
 
@@ -550,8 +554,22 @@ int bhrt_ctx_set_scene(bhrt_ctx* c, const bhrt_scene* s, bhrt_status_info* info)
     std::vector<unsigned long long> table;
     const bool cull = s->n_spheres > 0 && build_cull_table(s, k, table);
     const size_t cull_bytes = cull ? sizeof(unsigned long long) * table.size() : 0;
+    std::vector<float> sfr;  // KParams::sph_frame
+    if (cull) {
+        const HV3 a = hv(k.cull_a), b = hv(k.cull_b), e1 = hv(k.cam_e1);
+        for (int i = 0; i < s->n_spheres; ++i) {
+            const HV3 cc = hsub(hv(s->spheres[i].center), hv(s->center));
+            const double r = s->spheres[i].radius;
+            sfr.push_back(static_cast<float>(hdot(cc, a)));
+            sfr.push_back(static_cast<float>(hdot(cc, b)));
+            sfr.push_back(static_cast<float>(hdot(cc, e1)));
+            // fp32 slack: the device forms c.n, c.e2 from rounded floats
+            sfr.push_back(static_cast<float>(r + 1e-5 * (hnorm(cc) + r) + 1e-6));
+        }
+    }
+    const size_t sfr_bytes = sizeof(float) * sfr.size();
     const size_t chk_bytes = sizeof checker;
-    const size_t need = chk_bytes + sky_bytes + sph_bytes + cull_bytes;
+    const size_t need = chk_bytes + sky_bytes + sph_bytes + cull_bytes + sfr_bytes;
     c->upload_bytes = need;
     if (need > c->staging_cap) {
         if (c->staging) CK(cudaFreeHost(c->staging));
@@ -587,6 +605,11 @@ int bhrt_ctx_set_scene(bhrt_ctx* c, const bhrt_scene* s, bhrt_status_info* info)
             CK(cudaMemcpyAsync(c->cull.p, c->staging + off, cull_bytes, cudaMemcpyHostToDevice, c->up_stream));
             off += cull_bytes;
             k.cull = c->cull.p;
+            if (c->sph_frame.ensure(sfr.size())) return set_info(info, BHRT_DEVICE, -1, -1, "sphere alloc failed");
+            std::memcpy(c->staging + off, sfr.data(), sfr_bytes);
+            CK(cudaMemcpyAsync(c->sph_frame.p, c->staging + off, sfr_bytes, cudaMemcpyHostToDevice, c->up_stream));
+            off += sfr_bytes;
+            k.sph_frame = c->sph_frame.p;
         }
     }
     k.fused_shade = (32 % s->spp) == 0 ? 1 : 0;
@@ -606,7 +629,8 @@ int bhrt_ctx_set_scene(bhrt_ctx* c, const bhrt_scene* s, bhrt_status_info* info)
         const size_t E = static_cast<size_t>(s->table_entries);
         if (!c->has_table || std::memcmp(key, c->table_key, sizeof key) != 0) {
             if (c->tab_smp.ensure(E * s->table_samples * 2) || c->tab_ends.ensure(E * 4) ||
-                c->tab_kind.ensure(E) || c->tab_n.ensure(E) || c->tab_psi0.ensure(E))
+                c->tab_kind.ensure(E) || c->tab_n.ensure(E) || c->tab_psi0.ensure(E) ||
+                c->tab_meta.ensure(6 * E))
                 return set_info(info, BHRT_DEVICE, -1, -1, "table alloc failed");
             launch_table_build(k, c->tab_smp.p, c->tab_ends.p, c->tab_kind.p, c->tab_n.p, c->up_stream);
             CK(cudaGetLastError());
@@ -619,9 +643,10 @@ int bhrt_ctx_set_scene(bhrt_ctx* c, const bhrt_scene* s, bhrt_status_info* info)
         k.tab_kind = c->tab_kind.p;
         k.tab_n = c->tab_n.p;
         k.tab_psi0 = c->tab_psi0.p;
+        k.tab_meta = c->tab_meta.p;
         // bind the frame: each entry's inbound psi of the camera's u0 (oracle prep_table)
         const double u0 = 1.0 / hnorm(hsub(hv(s->cam_pos), hv(s->center)));
-        launch_table_bind(k, c->tab_ends.p, c->tab_psi0.p, u0, c->up_stream);
+        launch_table_bind(k, c->tab_ends.p, c->tab_psi0.p, c->tab_meta.p, u0, c->up_stream);
         CK(cudaGetLastError());
     }
     k.grow = c->tables.p;

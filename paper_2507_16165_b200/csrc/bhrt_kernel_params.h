@@ -75,6 +75,12 @@ struct KParams {
     const unsigned long long* cull;
     int32_t cull_bins, cull_words;
     double cull_a[3], cull_b[3];
+    // per-frame sphere records for the candidate prefilter, 4 floats per
+    // sphere: (c.a, c.b, c.e1, r + slack), c = centre - hole, a/b = cull_a/b,
+    // e1 = cam_e1. Every orbital plane n(theta) = cos(theta) b - sin(theta) a
+    // contains e1, so c.n and c.e2 are two fp32 fmas per sphere (conservative:
+    // the exact fp64 tests run in sphere_search)
+    const float* sph_frame;
     // 1: shade inside the trace kernel (spp divides 32; the spp samples of a
     // pixel are adjacent lanes, summed in sample order by warp shuffles)
     int32_t fused_shade;
@@ -91,6 +97,11 @@ struct KParams {
     const int32_t* tab_kind;
     const int32_t* tab_n;
     const double* tab_psi0;
+    // per-frame entry records (bind_table_kernel): everything a sample needs
+    // of an entry but its (u, u') samples, in one 48-byte record, so the two
+    // bracketing entries of a sample are three 16-byte loads each, issued
+    // together (table.cu TabMeta)
+    const void* tab_meta;
     int32_t table_entries, table_ns;
     double table_b_max, table_dpsi;
     double inv_table_b_max, inv_table_dpsi;  // RN(1/.) from the host (exact quotients: table.cu div_by)

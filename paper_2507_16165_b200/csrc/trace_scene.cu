@@ -13,6 +13,10 @@
 #ifndef BHRT_INL_SHADE
 #define BHRT_INL_SHADE __noinline__
 #endif
+// the escape direction out of line too (once per escaping ray): 7.27 -> 7.20 ms
+#ifndef BHRT_INL_ESC
+#define BHRT_INL_ESC __noinline__
+#endif
 #include "device_common.cuh"
 
 namespace bhrt_b200 {
@@ -76,6 +80,26 @@ __device__ __forceinline__ float atan2_cull(float y, float x) {
     if (ay > ax) r = 1.57079637f - r;
     if (x < 0.0f) r = 3.14159274f - r;
     return copysignf(r, y);
+}
+
+// The same window from fp32 inputs (the cull-table path): origin outside the
+// circle iff rc > rho (rho carries the record's slack, so a near-boundary
+// case falls to the infinite window).
+__device__ __forceinline__ void sphere_window_ff(float cx, float cy, float rcf, float rhof, float& lo, float& hi) {
+    if (!(rcf > rhof)) {
+        lo = -CUDART_INF_F;
+        hi = CUDART_INF_F;
+        return;
+    }
+    const float x = __fdividef(rhof, rcf);
+    const float a = x <= 0.5f ? x * (1.0f + 0.2f * x * x) * 1.0001f : 1.5708f;
+    const float pc = atan2_cull(cy, cx);
+    lo = pc - a - kWinMargin;
+    hi = pc + a + kWinMargin;
+    if (hi < 0.0f) {
+        lo += 2.0f * (float)PI_D;
+        hi += 2.0f * (float)PI_D;
+    }
 }
 
 // rcf = |(cx, cy)| and rhof = sqrt(rho2) in fp32 (shared with the radial extent)
@@ -160,13 +184,41 @@ __device__ BHRT_INL_SETUP double events_setup(const KParams& p, SM& sm, int t, V
         int bin = (int)(th * (float)(p.cull_bins / PI_D));
         bin = bin < 0 ? 0 : (bin >= p.cull_bins ? p.cull_bins - 1 : bin);
         const unsigned long long* row = p.cull + (size_t)bin * p.cull_words;
+        // Candidates in fp32 from the per-frame records (KParams::sph_frame):
+        // n = cos(t) b - sin(t) a and e2 = cos(t) a + sin(t) b with
+        // (cos t, sin t) = (n.b, -n.a), so c.n = na ca + nb cb and
+        // c.e2 = nb ca - na cb. A CONSERVATIVE superset of the oracle's exact
+        // |c.n| < r set (slack in the record's radius); sphere_search re-runs
+        // the exact fp64 test and the windows only cull, so results are the
+        // oracle's. Replaces four fp64 loads + two fp64 dots per sphere.
+        const float4* sf = reinterpret_cast<const float4*>(p.sph_frame);
         bool go = true;
         for (int w = 0; w < p.cull_words && go; ++w) {
             unsigned long long m = __ldg(row + w);
             while (m && go) {
                 const int k = w * 64 + __ffsll((long long)m) - 1;
                 m &= m - 1;
-                go = consider(k);
+                const float4 f = __ldg(sf + k);  // (ca, cb, cx, r + slack)
+                const float dn = fmaf(na, f.x, nb * f.y);
+                if (!(fabsf(dn) < f.w)) continue;
+                if (nc == kSlots) {
+                    nc = -1;
+                    go = false;
+                    break;
+                }
+                const float cx = f.z, cy = fmaf(nb, f.x, -na * f.y);
+                const float rho2 = fmaxf(fmaf(f.w, f.w, -dn * dn), 0.0f);  // >= r^2 - dn^2 (slack)
+                const float rc = sqrtf(fmaf(cx, cx, cy * cy)), rho = sqrtf(rho2);
+                float lo, hi;
+                sphere_window_ff(cx, cy, rc, rho, lo, hi);
+                sm.lo[nc][t] = lo;
+                sm.hi[nc][t] = hi;
+                sm.rlo[nc][t] = (rc - rho) - 1e-5f * (rc + rho);
+                sm.rhi[nc][t] = (rc + rho) * (1.0f + 1e-5f);
+                BHRT_ASSERT(k >= 0 && k < p.n_spheres && nc >= 0 && nc < kSlots);
+                sm.k[nc][t] = (unsigned char)k;
+                next_sph = fminf(next_sph, lo);
+                ++nc;
             }
         }
     } else {
