@@ -393,9 +393,13 @@ __device__ BHRT_INL_EVT bool step_events(const KParams& p, SM& sm, int t, double
     // ---- spheres
     const int nc = sm.nc[t];
     const bool test_all = nc < 0;
+    // No window starts by pb (next_sph = the smallest window start, passed
+    // windows already moved on): no candidate meets the step, none is passed,
+    // so the sphere half is skipped entirely — disk-only event steps.
+    const bool sph_here = test_all || sm.next_sph[t] <= (float)pb;
     unsigned act = 0;
     unsigned ang = 0;  // candidates whose angular window meets the step
-    if (!test_all) {
+    if (!test_all && sph_here) {
         const float fa = (float)pa, fb = (float)pb;
         for (int i = 0; i < nc; ++i)
             if (sm.lo[i][t] <= fb && sm.hi[i][t] >= fa) ang |= 1u << i;
@@ -490,7 +494,7 @@ __device__ BHRT_INL_EVT bool step_events(const KParams& p, SM& sm, int t, double
         sm.sigma[t] = sg;
     }
     float next_sph = sm.next_sph[t];
-    if (!test_all) {
+    if (!test_all && sph_here) {
         next_sph = CUDART_INF_F;
         const float fb = (float)pb;
         for (int i = 0; i < nc; ++i) {
@@ -668,8 +672,17 @@ __global__ void __launch_bounds__(kBlock, BHRT_SCENE_MINB) trace_scene_kernel(co
                     H.obj = BHRT_OBJ_SKY;
                     H.point = escape_dir(p, sm, t, false, 0.0, 0.0, 0.0, phi, u, w);
                 } else {
+                    // One combined test per accepted step covers the common
+                    // case — no event, capture, escape, numerical failure,
+                    // underflow or stall can follow: pn below the next event
+                    // angle and phi_max, un strictly inside (u_esc, u_cap)
+                    // (so un > 0), hn >= 1e-14 — and commits the step. Any
+                    // other outcome takes the exact tests in their original
+                    // order below; the stall test of the next trip is
+                    // evaluated at the end of this one (phi is unchanged by
+                    // a rejection, and phi = 0 < phi_max on entry).
+                    double nev_eff = dmin(next_ev, p.phi_max);
                     for (;;) {
-                        if (phi > p.phi_max) { H.obj = BHRT_OBJ_STALLED; break; }
                         double un, wn, hn;
                         // controller factors straight from the (L1-resident) global tables: measured
                         // faster than staging them in shared memory (8.21 -> 8.05 ms, config 2)
@@ -677,10 +690,18 @@ __global__ void __launch_bounds__(kBlock, BHRT_SCENE_MINB) trace_scene_kernel(co
                                        wn, hn)) {
                             const double pn = phi + h;
                             ++nsteps;
+                            if (pn < nev_eff && un > p.u_esc && un < p.u_cap && hn >= 1e-14) {
+                                phi = pn;
+                                u = un;
+                                w = wn;
+                                h = hn;
+                                continue;
+                            }
                             if (pn >= next_ev && step_events(p, sm, t, phi, u, w, pn, un, wn, next_ev, H)) {
                                 phi = pn;
                                 break;
                             }
+                            nev_eff = dmin(next_ev, p.phi_max);
                             if (!(un > 0.0)) {
                                 H.obj = -BHRT_NUMERICAL;
                                 if (DIAG) H.point = mk(un, 1.0, 0.0);
@@ -713,6 +734,7 @@ __global__ void __launch_bounds__(kBlock, BHRT_SCENE_MINB) trace_scene_kernel(co
                             if (DIAG && H.obj < 0) H.point = mk(u, 2.0, 0.0);
                             break;
                         }
+                        if (phi > p.phi_max) { H.obj = BHRT_OBJ_STALLED; break; }
                     }
                 }
             }
