@@ -459,9 +459,18 @@ def run_ours(args):
     from paper_2507_16165_b200.parallel import FrameRenderer
 
     rank, world, local = env_rank()
+    # BHRT_BENCH_SHARED_GPU=1 (tests only): every rank on cuda:0 over gloo, to
+    # exercise the N > 1 control flow (collective order, no deadlock) on a
+    # one-GPU lease; never a timing configuration
+    shared = os.environ.get("BHRT_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     scene = scenes.config(args.config)
     W, H, spp = scene.s.width, scene.s.height, scene.s.spp
     total_rays = W * H * spp
@@ -549,13 +558,22 @@ def run_ours(args):
                   "api": "bhrt_cuda_render_rows (C ABI; render_shim.cpp render_rows), host buffers",
                   "image_equals_frame_renderer": same}
 
+    # ---- roofline denominator (every rank measures its own GPU)
+    peak = native.lib().bhrt_b200_fp64_peak_tflops(200000, 3, None)
+
+    # ---- the other BASELINE.json configs (secondary lines). Called on EVERY
+    # rank: config 4's frames are sharded over the ranks (its barrier and
+    # max-over-ranks reduction are collectives); the rest runs on rank 0.
+    secondary = None
+    if not args.no_secondary:
+        secondary = measure_secondary(local, peak, rank=rank, world=world)
+
     if rank != 0:
         dist.barrier() if world > 1 else None
         dist.destroy_process_group() if world > 1 else None
         return 0
 
     # ---- roofline of the dominant kernel (trace), FP64 pipe
-    peak = native.lib().bhrt_b200_fp64_peak_tflops(200000, 3, None)
     avg_trace_ms = sum(trace_ms) / len(trace_ms)
     achieved = (sum(flops) / len(flops)) / (avg_trace_ms * 1e-3) / 1e12
     traffic = None
@@ -568,11 +586,6 @@ def run_ours(args):
             pipe_busy = tj.get(f"config{args.config}_fp64_pipe_active")
         except Exception:
             traffic = None
-
-    # ---- the other BASELINE.json configs (secondary lines, rank 0, this GPU)
-    secondary = None
-    if not args.no_secondary:
-        secondary = measure_secondary(local, peak, rank=rank, world=world)
 
     # ---- CPU baseline on this box's host cores (rank 0, N=1 only)
     cpu = None

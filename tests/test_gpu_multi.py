@@ -203,3 +203,29 @@ def test_bench_two_gpus_self_launch():
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
     assert len(lines) == 1 and lines[0]["n_gpus"] == 2 and lines[0]["value"] > 0
+
+
+def test_bench_two_ranks_control_flow_on_one_gpu():
+    """bench.py under torchrun with 2 ranks (BHRT_BENCH_SHARED_GPU: both on
+    cuda:0 over gloo — control flow only, never a timing): every collective
+    of the timed steps, the e2e loop and the secondary lines (config 4's
+    frames are sharded over the ranks) matches up, no rank hangs, rank 0
+    prints one line with n_gpus = 2."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ, BHRT_BENCH_SHARED_GPU="1")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                        "--master-addr", "127.0.0.1", f"--master-port={port}",
+                        os.path.join(root, "bench.py"), "--gpus", "2", "--steps", "2", "--warmup", "3",
+                        "--no-cpu"], cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1
+    d = lines[0]
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["secondary"]["config4"]["n_gpus"] == 2
