@@ -196,6 +196,42 @@ __device__ __forceinline__ void initial_conditions(const KParams& p, V3 dir, dou
     w = -dot(v, dir) / (p.cam_r0 * b);
 }
 
+// atan2 for the disk-line angle of the scene modes: t =
+// min/max of |x|, |y| (one division), atan(t) = t + t s Q(s), s = t^2, with
+// Q a degree-19 Chebyshev fit (mpmath, |rel err| < 2.3e-16 on [0, 1])
+// evaluated by Estrin's scheme (8 dependent operations instead of 19 for
+// Horner), then the octant fix-up with two-part pi/2, pi. Normative op order
+// (oracle/bhrt_oracle.c atan2_est = device_common.cuh atan2_est). Finite
+// arguments, not both zero.
+__device__ __forceinline__ double atan2_est(double y, double x) {
+    const double ax = fabs(x), ay = fabs(y);
+    const double mx = ax < ay ? ay : ax, mn = ax < ay ? ax : ay;
+    const double t = mn / mx;
+    const double s = t * t, s2 = s * s, s4 = s2 * s2, s8 = s4 * s4, s16 = s8 * s8;
+    const double b0 = fma(0x1.9999999999620p-3, s, -0x1.5555555555555p-2);
+    const double b1 = fma(0x1.c71c71bb00a6cp-4, s, -0x1.24924924753ecp-3);
+    const double b2 = fma(0x1.3b1399d1dcdc7p-4, s, -0x1.745d15ee35819p-4);
+    const double b3 = fma(0x1.e1d0239d392a6p-5, s, -0x1.110fff599e4d2p-4);
+    const double b4 = fma(0x1.841dcf603a209p-5, s, -0x1.aebbb1647a168p-5);
+    const double b5 = fma(0x1.3328700bb8169p-5, s, -0x1.5d02278205cc7p-5);
+    const double b6 = fma(0x1.843f4bca23369p-6, s, -0x1.00390504e9f2fp-5);
+    const double b7 = fma(0x1.123baedb61abdp-7, s, -0x1.fd0e4de8fed90p-7);
+    const double b8 = fma(0x1.1325b2f8964bep-10, s, -0x1.ca3677db66678p-9);
+    const double b9 = fma(0x1.2f07811f9f6e9p-16, s, -0x1.a359b96a4eee4p-13);
+    const double d0 = fma(b1, s2, b0);
+    const double d1 = fma(b3, s2, b2);
+    const double d2 = fma(b5, s2, b4);
+    const double d3 = fma(b7, s2, b6);
+    const double d4 = fma(b9, s2, b8);
+    const double e0 = fma(d1, s4, d0), e1 = fma(d3, s4, d2);
+    const double g0 = fma(e1, s8, e0);
+    const double q = fma(d4, s16, g0);
+    double r = fma(t * s, q, t);
+    if (ay > ax) r = (0x1.921fb54442d18p+0 - r) + 0x1.1a62633145c07p-54;
+    if (x < 0.0) r = (0x1.921fb54442d18p+1 - r) + 0x1.1a62633145c07p-53;
+    return copysign(r, y);
+}
+
 // ----------------------------------------------------------------- record / stats helpers
 // Per-warp counter totals, one 64-bit atomic per counter from lane 0. The
 // per-lane counts are 32-bit; while every lane's count is below 2^26 the

@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(128, BHRT_TAB_MINB) trace_table_kernel(const _
             }
             point = obj == BHRT_OBJ_SKY ? dir : add(origin, scl(dir, best));
         } else {
-            const V3 e1 = vld(p.cam_e1), e2 = F.e2, nrm = cross(e1, e2);
+            const V3 e1 = vld(p.cam_e1), e2 = F.e2;
             const double u0 = p.cam_u0, w0 = F.w;
             const double M2 = 2.0 * p.mass;
             const double energy = w0 * w0 + u0 * u0 - M2 * u0 * u0 * u0;
@@ -335,15 +335,14 @@ __global__ void __launch_bounds__(128, BHRT_TAB_MINB) trace_table_kernel(const _
                 double next_disk = CUDART_INF, sigma = 1.0;
                 V3 Lw = mk(0.0, 0.0, 0.0);
                 if (p.disk_enabled) {
-                    const V3 L = mk(-nrm.z, 0.0, nrm.x);
-                    const double nl2 = dot(L, L);
+                    const double lx = -e2.y, ly = e1.y;  // (L.e1, L.e2), oracle ray_events_setup
+                    const double nl2 = lx * lx + ly * ly;
                     if (nl2 >= 1e-24) {  // |L| >= 1e-12
                         const double nl = sqrt(nl2);
-                        const double lx = dot(L, e1), ly = dot(L, e2);
-                        const double pl = atan2(ly, lx);
+                        const double pl = atan2_est(ly, lx);
                         next_disk = pl > 0.0 ? pl : pl + PI_D;
                         sigma = pl > 0.0 ? 1.0 : -1.0;
-                        Lw = dvd(L, nl);
+                        Lw = dvd(add(scl(e1, lx), scl(e2, ly)), nl);
                     }
                 }
                 const int N = p.table_entries;

@@ -21,6 +21,7 @@
 
 namespace bhrt_b200 {
 
+
 #ifndef BHRT_SCENE_BLOCK
 #define BHRT_SCENE_BLOCK 128
 #endif
@@ -133,10 +134,11 @@ __device__ BHRT_INL_SETUP double events_setup(const KParams& p, SM& sm, int t, V
     double next_disk = CUDART_INF;
     sm.sigma[t] = 1.0;
     if (p.disk_enabled) {
-        const V3 L = mk(-n.z, 0.0, n.x);
-        if (dot(L, L) >= 1e-24) {  // |L| >= 1e-12 (oracle ray_events_setup)
-            const double lx = dot(L, e1), ly = dot(L, e2);
-            const double pl = atan2(ly, lx);
+        // the disk line in plane coordinates: (L.e1, L.e2) = (-e2.y, e1.y)
+        // (oracle ray_events_setup)
+        const double lx = -e2.y, ly = e1.y;
+        if (lx * lx + ly * ly >= 1e-24) {  // |L| >= 1e-12
+            const double pl = atan2_est(ly, lx);
             next_disk = pl > 0.0 ? pl : pl + PI_D;
             sm.sigma[t] = pl > 0.0 ? 1.0 : -1.0;
             // the unit line (lx/nl, ly/nl) and L/nl are formed at hit time (disk_line)
@@ -254,12 +256,12 @@ struct Hit {
 // values, same operations), formed only when a disk crossing lands in the annulus.
 template <class SM>
 __device__ __forceinline__ void disk_line(const KParams& p, const SM& sm, int t, double& dlx, double& dly, V3& Lw) {
-    const V3 n = ld3(sm.n, t), e1 = vld(p.cam_e1), e2 = ld3(sm.e2, t);
-    const V3 L = mk(-n.z, 0.0, n.x);
-    const double nl = norm(L);
-    dlx = dot(L, e1) / nl;
-    dly = dot(L, e2) / nl;
-    Lw = dvd(L, nl);
+    const V3 e1 = vld(p.cam_e1), e2 = ld3(sm.e2, t);
+    const double lx = -e2.y, ly = e1.y;
+    const double nl = sqrt(lx * lx + ly * ly);
+    dlx = lx / nl;
+    dly = ly / nl;
+    Lw = dvd(add(scl(e1, lx), scl(e2, ly)), nl);
 }
 
 // Sphere half of step_events(): first entering hit on the step's S
