@@ -521,6 +521,12 @@ int bhrt_ctx_set_scene(bhrt_ctx* c, const bhrt_scene* s, bhrt_status_info* info)
     k.height = s->height;
     k.spp = s->spp;
     k.seed = s->seed;
+    {  // camera.cpp:12-17 splitmix64 of the seed (hash_counter's first round)
+        uint64_t x = s->seed + 0x9e3779b97f4a7c15ULL;
+        x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+        x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+        k.seed_mix = x ^ (x >> 31);
+    }
     k.epsilon = s->epsilon;
     k.rel_tol = s->rel_tol;
     k.abs_tol = s->abs_tol;

@@ -37,6 +37,7 @@ struct KParams {
     int32_t width, height, spp;
     int32_t diag;  // 1: failed samples carry (u, kind) in their record (bhrt_cuda.cu failure_text)
     uint64_t seed;
+    uint64_t seed_mix;  // splitmix64(seed): hash_counter's first round (camera.cpp:21-28), per frame
     // integrator
     double epsilon, rel_tol, abs_tol, step, max_step, chord_dphi;
     // mode R: pow(1e-4, 0.4 / 5) with the HOST libm, i.e. the value the

@@ -60,19 +60,16 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
     return x ^ (x >> 31);
 }
 __device__ __forceinline__ double to_unit(uint64_t h) { return (double)(h >> 11) * 0x1.0p-53; }
-__device__ __forceinline__ uint64_t hash_counter(uint64_t seed, uint64_t a, uint64_t b, uint64_t c) {
-    uint64_t h = splitmix64(seed);
-    h = splitmix64(h ^ a);
-    h = splitmix64(h ^ b);
-    h = splitmix64(h ^ c);
-    return h;
-}
 
 __device__ __forceinline__ V3 camera_dir_raw(const KParams& p, int px, int py, int sample) {
     double sx = 0.5, sy = 0.5;
     if (p.spp > 1) {
-        sx = to_unit(hash_counter(p.seed, (uint64_t)px, (uint64_t)py, 2 * (uint64_t)sample));
-        sy = to_unit(hash_counter(p.seed, (uint64_t)px, (uint64_t)py, 2 * (uint64_t)sample + 1));
+        // hash_counter(seed, px, py, 2s [+1]) (camera.cpp:21-28): the first
+        // round is the per-frame KParams::seed_mix = splitmix64(seed), the
+        // next two are shared by the sample's x and y offsets
+        const uint64_t h = splitmix64(splitmix64(p.seed_mix ^ (uint64_t)px) ^ (uint64_t)py);
+        sx = to_unit(splitmix64(h ^ (2 * (uint64_t)sample)));
+        sy = to_unit(splitmix64(h ^ (2 * (uint64_t)sample + 1)));
     }
     // (px + sx) / width as RN(a y) plus one Markstein correction with the
     // host's y = RN(1/width): the correctly rounded quotient for these

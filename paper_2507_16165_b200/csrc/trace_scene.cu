@@ -631,29 +631,55 @@ __global__ void __launch_bounds__(kBlock, BHRT_SCENE_MINB) trace_scene_kernel(co
             bool has_step = false;
             if (INTEG == BHRT_INTEGRATOR_RK4) {
                 const double h = p.step;
-                for (;;) {  // tests/oracles.hpp:47-54 loop structure
-                    if (!(phi < p.phi_max)) { H.obj = BHRT_OBJ_STALLED; break; }
-                    if (u >= p.u_cap) { H.obj = BHRT_OBJ_HORIZON; break; }
-                    if (u <= p.u_esc && w < 0.0) { H.obj = BHRT_OBJ_SKY; break; }
-                    double un, wn;
-                    rk4_step(u, w, h, p.mass, un, wn);
-                    const double pn = phi + h;
-                    ++nsteps;
-                    if (pn >= next_ev && step_events(p, sm, t, phi, u, w, pn, un, wn, next_ev, H)) {
+                // tests/oracles.hpp:47-54 loop structure (budget, capture and
+                // escape tested before each step). The tests of the next trip
+                // follow the step that produced the state; one combined test
+                // (pn below the next event angle and phi_max, un strictly in
+                // (u_esc, u_cap)) commits the common step, which none of them
+                // can stop.
+                if (!(phi < p.phi_max)) {
+                    H.obj = BHRT_OBJ_STALLED;
+                } else if (u >= p.u_cap) {
+                    H.obj = BHRT_OBJ_HORIZON;
+                } else if (u <= p.u_esc && w < 0.0) {
+                    H.obj = BHRT_OBJ_SKY;
+                } else {
+                    double nev_eff = dmin(next_ev, p.phi_max);
+                    for (;;) {
+                        double un, wn;
+                        rk4_step(u, w, h, p.mass, un, wn);
+                        const double pn = phi + h;
+                        ++nsteps;
+                        if (pn < nev_eff && un > p.u_esc && un < p.u_cap) {
+                            pp = phi;
+                            up = u;
+                            wp = w;
+                            has_step = true;
+                            phi = pn;
+                            u = un;
+                            w = wn;
+                            continue;
+                        }
+                        if (pn >= next_ev && step_events(p, sm, t, phi, u, w, pn, un, wn, next_ev, H)) {
+                            phi = pn;
+                            break;
+                        }
+                        nev_eff = dmin(next_ev, p.phi_max);
+                        pp = phi;
+                        up = u;
+                        wp = w;
+                        has_step = true;
                         phi = pn;
-                        break;
-                    }
-                    pp = phi;
-                    up = u;
-                    wp = w;
-                    has_step = true;
-                    phi = pn;
-                    u = un;
-                    w = wn;
-                    if (!(u > 0.0)) {
-                        H.obj = -BHRT_NUMERICAL;
-                        if (DIAG) H.point = mk(u, 1.0, 0.0);
-                        break;
+                        u = un;
+                        w = wn;
+                        if (!(u > 0.0)) {
+                            H.obj = -BHRT_NUMERICAL;
+                            if (DIAG) H.point = mk(u, 1.0, 0.0);
+                            break;
+                        }
+                        if (!(phi < p.phi_max)) { H.obj = BHRT_OBJ_STALLED; break; }
+                        if (u >= p.u_cap) { H.obj = BHRT_OBJ_HORIZON; break; }
+                        if (u <= p.u_esc && w < 0.0) { H.obj = BHRT_OBJ_SKY; break; }
                     }
                 }
             } else {
