@@ -22,7 +22,7 @@ namespace bhrt_b200 {
 
 int launch_trace(const KParams& p, cudaStream_t st, int* launches, cudaEvent_t* ev);
 void launch_table_build(const KParams& p, double* smp, double* ends, int32_t* kind, int32_t* n, cudaStream_t st);
-void launch_table_bind(const KParams& p, double* ends, double* psi0, void* meta, double u0, cudaStream_t st);
+void launch_table_bind(const KParams& p, double* ends, double* psi0, double u0, cudaStream_t st);
 void launch_trace_polylines(const KParams& p, const double* rays, long long n, bhrt_ray_record* records,
                             double* pts, int cap, int* npoly, cudaStream_t st);
 void launch_trace_rays(const KParams& p, const double* rays, long long n, bhrt_ray_record* records,
@@ -217,7 +217,6 @@ struct bhrt_ctx {
     DevBuf<float> sph_frame;  // KParams::sph_frame
     DevBuf<double> tab_smp, tab_ends, tab_psi0;
     DevBuf<int32_t> tab_kind, tab_n;
-    DevBuf<double> tab_meta;  // 6 doubles (48 B) per entry: table.cu TabMeta
     bool has_table = false;
     double table_key[10] = {0};
     cudaStream_t last_stream = nullptr;
@@ -468,7 +467,6 @@ void bhrt_ctx_destroy(bhrt_ctx* c) {
     c->tab_psi0.release();
     c->tab_kind.release();
     c->tab_n.release();
-    c->tab_meta.release();
     delete c;
 }
 
@@ -635,8 +633,7 @@ int bhrt_ctx_set_scene(bhrt_ctx* c, const bhrt_scene* s, bhrt_status_info* info)
         const size_t E = static_cast<size_t>(s->table_entries);
         if (!c->has_table || std::memcmp(key, c->table_key, sizeof key) != 0) {
             if (c->tab_smp.ensure(E * s->table_samples * 2) || c->tab_ends.ensure(E * 4) ||
-                c->tab_kind.ensure(E) || c->tab_n.ensure(E) || c->tab_psi0.ensure(E) ||
-                c->tab_meta.ensure(6 * E))
+                c->tab_kind.ensure(E) || c->tab_n.ensure(E) || c->tab_psi0.ensure(E))
                 return set_info(info, BHRT_DEVICE, -1, -1, "table alloc failed");
             launch_table_build(k, c->tab_smp.p, c->tab_ends.p, c->tab_kind.p, c->tab_n.p, c->up_stream);
             CK(cudaGetLastError());
@@ -649,10 +646,9 @@ int bhrt_ctx_set_scene(bhrt_ctx* c, const bhrt_scene* s, bhrt_status_info* info)
         k.tab_kind = c->tab_kind.p;
         k.tab_n = c->tab_n.p;
         k.tab_psi0 = c->tab_psi0.p;
-        k.tab_meta = c->tab_meta.p;
         // bind the frame: each entry's inbound psi of the camera's u0 (oracle prep_table)
         const double u0 = 1.0 / hnorm(hsub(hv(s->cam_pos), hv(s->center)));
-        launch_table_bind(k, c->tab_ends.p, c->tab_psi0.p, c->tab_meta.p, u0, c->up_stream);
+        launch_table_bind(k, c->tab_ends.p, c->tab_psi0.p, u0, c->up_stream);
         CK(cudaGetLastError());
     }
     k.grow = c->tables.p;

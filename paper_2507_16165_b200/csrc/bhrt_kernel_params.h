@@ -98,11 +98,6 @@ struct KParams {
     const int32_t* tab_kind;
     const int32_t* tab_n;
     const double* tab_psi0;
-    // per-frame entry records (bind_table_kernel): everything a sample needs
-    // of an entry but its (u, u') samples, in one 48-byte record, so the two
-    // bracketing entries of a sample are three 16-byte loads each, issued
-    // together (table.cu TabMeta)
-    const void* tab_meta;
     int32_t table_entries, table_ns;
     double table_b_max, table_dpsi;
     double inv_table_b_max, inv_table_dpsi;  // RN(1/.) from the host (exact quotients: table.cu div_by)

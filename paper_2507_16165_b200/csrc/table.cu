@@ -95,35 +95,12 @@ __device__ double inbound_psi(const TabView& T, int e, double target) {
     return (double)j * T.dpsi + h * t;
 }
 
-// Per-frame entry record (bind_table_kernel): the frame's inbound psi of
-// the camera's u0, the entry's ends {psi_end, u_end, w_end, psi_esc}, kind
-// and sample count — one 48-byte record, read as three 16-byte loads.
-struct __align__(16) TabMeta {
-    double psi0, psi_end, u_end, w_end, psi_esc;
-    int32_t kind, n;
-};
-static_assert(sizeof(TabMeta) == 48, "TabMeta layout");
-
-__device__ __forceinline__ TabMeta load_meta(const KParams& p, int e) {
-    const double2* m = reinterpret_cast<const double2*>(p.tab_meta) + 3 * (size_t)e;
-    const double2 a = __ldg(m), b = __ldg(m + 1), c = __ldg(m + 2);
-    TabMeta t;
-    t.psi0 = a.x;
-    t.psi_end = a.y;
-    t.u_end = b.x;
-    t.w_end = b.y;
-    t.psi_esc = c.x;
-    const long long kn = __double_as_longlong(c.y);
-    t.kind = (int32_t)(unsigned)(kn & 0xffffffffll);
-    t.n = (int32_t)(kn >> 32);
-    return t;
-}
-
 // oracle table_u: u on entry e at orbit angle psi (mirrored past periapsis).
-__device__ double table_u(const TabView& T, const TabMeta& M, int e, double psi) {
-    const int kind = M.kind, n = M.n;
+__device__ double table_u(const TabView& T, int e, double psi) {
+    const int kind = __ldg(&T.kind[e]), n = __ldg(&T.n[e]);
     const double* S = T.smp + (size_t)e * T.ns * 2;
-    const double pend = M.psi_end;
+    const double* E = T.ends + 4 * (size_t)e;
+    const double pend = __ldg(&E[0]);
     if (kind == 1 && psi > pend) psi = 2.0 * pend - psi;
     if (psi < 0.0 || n < 1) return -1.0;
     int j = (int)floor(div_by(psi, T.dpsi, T.inv_dpsi));
@@ -133,11 +110,11 @@ __device__ double table_u(const TabView& T, const TabMeta& M, int e, double psi)
         j = n - 1;
         pa = (double)j * T.dpsi;
         h = pend - pa;
-        if (!(h > 0.0)) return M.u_end;
+        if (!(h > 0.0)) return __ldg(&E[1]);
         ua = __ldg(&S[2 * j]);
         wa = __ldg(&S[2 * j + 1]);
-        ub = M.u_end;
-        wb = M.w_end;
+        ub = __ldg(&E[1]);
+        wb = __ldg(&E[2]);
     } else {
         pa = (double)j * T.dpsi;
         h = T.dpsi;
@@ -234,40 +211,27 @@ __global__ void __launch_bounds__(128) build_table_kernel(const __grid_constant_
     E[3] = -1.0;
 }
 
-// psi_esc per entry (needs the finished entry) and, per frame, psi0 of u0
-// and the entry records (TabMeta).
-__global__ void bind_table_kernel(const __grid_constant__ KParams p, double* ends, double* psi0, TabMeta* meta,
+// psi_esc per entry (needs the finished entry) and, per frame, psi0 of u0.
+__global__ void bind_table_kernel(const __grid_constant__ KParams p, double* ends, double* psi0,
                                   double u0, int with_esc) {
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= p.table_entries) return;
     TabView T{p.tab_smp, ends, p.tab_kind, p.tab_n, p.table_ns, p.table_dpsi, 1.0 / p.table_dpsi};
     if (with_esc) ends[4 * (size_t)e + 3] = inbound_psi(T, e, p.u_esc);
-    if (psi0) {
-        const double q = inbound_psi(T, e, u0);
-        psi0[e] = q;
-        TabMeta m;
-        const double* E = ends + 4 * (size_t)e;
-        m.psi0 = q;
-        m.psi_end = E[0];
-        m.u_end = E[1];
-        m.w_end = E[2];
-        m.psi_esc = E[3];
-        m.kind = p.tab_kind[e];
-        m.n = p.tab_n[e];
-        meta[e] = m;
-    }
+    if (psi0) psi0[e] = inbound_psi(T, e, u0);
 }
 
 // oracle table_plan
-__device__ __forceinline__ bool table_plan(const TabMeta& M, double w0, int& outcome, double& phi_end) {
-    const int kind = M.kind;
-    const double psi0 = M.psi0;
+__device__ __forceinline__ bool table_plan(const TabView& T, int e, double psi0, double w0, int& outcome,
+                                           double& phi_end) {
+    const int kind = __ldg(&T.kind[e]);
+    const double* E = T.ends + 4 * (size_t)e;
     if (kind == 3 || psi0 < 0.0) return false;
-    const double pesc = M.psi_esc;
+    const double pesc = __ldg(&E[3]);
     if (w0 >= 0.0) {
         if (kind == 0) {
             outcome = BHRT_OBJ_HORIZON;
-            phi_end = M.psi_end - psi0;
+            phi_end = __ldg(&E[0]) - psi0;
             return true;
         }
         if (kind == 2) {
@@ -277,7 +241,7 @@ __device__ __forceinline__ bool table_plan(const TabMeta& M, double w0, int& out
         }
         if (pesc < 0.0) return false;
         outcome = BHRT_OBJ_SKY;
-        phi_end = (2.0 * M.psi_end - pesc) - psi0;
+        phi_end = (2.0 * __ldg(&E[0]) - pesc) - psi0;
         return true;
     }
     if (pesc < 0.0) return false;
@@ -351,13 +315,12 @@ __global__ void __launch_bounds__(128, BHRT_TAB_MINB) trace_table_kernel(const _
                 if (ie > N - 2) ie = N - 2;
                 BHRT_ASSERT(ie >= 0 && ie + 1 < N);
                 double f = x - (double)ie;
-                const TabMeta mi = load_meta(p, ie), mj = load_meta(p, ie + 1);
-                if (mi.kind == 3) f = 1.0;
-                const double p0i = mi.psi0, p0j = mj.psi0;
+                if (__ldg(&p.tab_kind[ie]) == 3) f = 1.0;
+                const double p0i = __ldg(&p.tab_psi0[ie]), p0j = __ldg(&p.tab_psi0[ie + 1]);
                 int oi = 0, oj = 0;
                 double pi_ = 0.0, pj = 0.0;
-                const bool vi = table_plan(mi, w0, oi, pi_);
-                const bool vj = table_plan(mj, w0, oj, pj);
+                const bool vi = table_plan(T, ie, p0i, w0, oi, pi_);
+                const bool vj = table_plan(T, ie + 1, p0j, w0, oj, pj);
                 int outcome = BHRT_OBJ_STALLED;
                 double phi_end = 0.0, wi = 0.0, wj = 0.0;
                 bool ok = true;
@@ -389,8 +352,8 @@ __global__ void __launch_bounds__(128, BHRT_TAB_MINB) trace_table_kernel(const _
                     while (next_disk < stop) {
                         const double ph = next_disk;
                         double ui = -1.0, uj = -1.0;
-                        if (wi > 0.0) ui = table_u(T, mi, ie, p0i + sgn * ph);
-                        if (wj > 0.0) uj = table_u(T, mj, ie + 1, p0j + sgn * ph);
+                        if (wi > 0.0) ui = table_u(T, ie, p0i + sgn * ph);
+                        if (wj > 0.0) uj = table_u(T, ie + 1, p0j + sgn * ph);
                         nevals += (wi > 0.0) + (wj > 0.0);
                         double u_ev;
                         if (wi > 0.0 && wj > 0.0 && ui >= 0.0 && uj >= 0.0)
@@ -437,12 +400,11 @@ void launch_table_build(const KParams& p, double* smp, double* ends, int32_t* ki
     q.tab_smp = smp;
     q.tab_kind = kind;
     q.tab_n = n;
-    bind_table_kernel<<<(p.table_entries + 255) / 256, 256, 0, st>>>(q, ends, nullptr, nullptr, 0.0, 1);
+    bind_table_kernel<<<(p.table_entries + 255) / 256, 256, 0, st>>>(q, ends, nullptr, 0.0, 1);
 }
 
-void launch_table_bind(const KParams& p, double* ends, double* psi0, void* meta, double u0, cudaStream_t st) {
-    bind_table_kernel<<<(p.table_entries + 255) / 256, 256, 0, st>>>(p, ends, psi0, static_cast<TabMeta*>(meta),
-                                                                       u0, 0);
+void launch_table_bind(const KParams& p, double* ends, double* psi0, double u0, cudaStream_t st) {
+    bind_table_kernel<<<(p.table_entries + 255) / 256, 256, 0, st>>>(p, ends, psi0, u0, 0);
 }
 
 void launch_table_trace(const KParams& p, cudaStream_t st) {

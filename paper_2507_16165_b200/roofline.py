@@ -10,11 +10,18 @@ per step attempt (accepted or rejected):
                    + scales 4 + guard 1 + h update 1 + phi update 1
   RK4        39  = 4 rhs x 3 + stage inputs 12 + combination 14 + phi 1
   REFERENCE 152  = DOPRI5 step incl. error norm and PI control
-per ray (scene modes): camera ray 31 + plane basis 38 + initial
-  conditions 33 + plane normal 9 + disk line 16. Sphere candidate tests are
-not counted (the kernel's plane-angle cull table skips most of the oracle's
-per-sphere |c.n| < r tests), nor are event (polyline hit-test) and shading
-arithmetic, so the achieved figure is a lower bound.
+per ray (counted from the kernels' normative operation order, round 2):
+  scene modes (RK4 / RKF45) 79 = raw camera direction 30 (u, v with the
+    reciprocal correction, the three-vector sum) + orbital frame 29
+    (scene_frame: dots, |T|^2, |D|^2 test, sqrt, one reciprocal, e2, u0')
+    + plane normal 9 + first integral 8 + disk-line norm test 3;
+  REFERENCE 81 = unit camera ray 39 (normalize: 3 divisions) + plane_basis
+    20 + initial_conditions 22 (geodesic.cpp:49-65).
+Transcendentals (the disk-line atan2 — an explicit Estrin polynomial in
+these kernels — sin/cos, asin, pow) are not counted, nor are the fp32
+culling arithmetic, the event steps' interpolation (13 flops each, about 2
+per ray on config 2), the escape tangent (about 87) and shading (about 15
+per sample): the achieved figure is a lower bound.
 """
 from __future__ import annotations
 
@@ -26,8 +33,8 @@ STEP_FLOPS = {INTEGRATOR_RKF45: 137.0, INTEGRATOR_RK4: 39.0, INTEGRATOR_REFERENC
 def setup_flops(scene) -> float:
     s = scene.s if hasattr(scene, "s") else scene
     if s.integrator == INTEGRATOR_REFERENCE:
-        return 31.0 + 38.0 + 33.0
-    return 31.0 + 38.0 + 33.0 + 9.0 + (16.0 if s.disk_enabled else 0.0)
+        return 39.0 + 20.0 + 22.0
+    return 30.0 + 29.0 + 9.0 + 8.0 + (3.0 if s.disk_enabled else 0.0)
 
 
 def launch_flops(scene, stats: dict) -> float:
