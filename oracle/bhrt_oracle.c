@@ -608,8 +608,9 @@ static int rkf45_step(double u, double w, double h, double M3, double rtol, doub
     sw = H1 * kw1; sw = fma(H3, kw3, sw); sw = fma(H4, kw4, sw); sw = fma(H5, kw5, sw);
     sw = fma(H6, kw6, sw);
     const double eu = fabs(h * su), ew = fabs(h * sw);
-    const double du = fma(rtol, fmax(fabs(u), fabs(u_new)), atol);
-    const double dw = fma(rtol, fmax(fabs(w), fabs(w_new)), atol);
+    /* max/min by compare-select (dmax/dmin: the first operand on NaN) */
+    const double du = fma(rtol, dmax(fabs(u), fabs(u_new)), atol);
+    const double dw = fma(rtol, dmax(fabs(w), fabs(w_new)), atol);
     /* error test, plus a geometric guard: one step may at most double r
      * (u_new >= u/2), so steps never overshoot past u = 0 on near-radial
      * outgoing rays (the reference's epsilon windows bound chords the same
@@ -625,7 +626,7 @@ static int rkf45_step(double u, double w, double h, double M3, double rtol, doub
     if (accept) {
         *un = u_new;
         *wn = w_new;
-        *hn = fmin(h * g_grow[q - QMIN], hmax);
+        *hn = dmin(h * g_grow[q - QMIN], hmax);
     } else if (err_ok) {
         *hn = 0.5 * h;
     } else {

@@ -547,20 +547,23 @@ __device__ __forceinline__ bool rkf45_step(double u, double w, double h, double 
     su = fma(H6, ku6, su);
     sw = H1 * kw1; sw = fma(H3, kw3, sw); sw = fma(H4, kw4, sw); sw = fma(H5, kw5, sw);
     sw = fma(H6, kw6, sw);
-    const double eu = fabs(h * su), ew = fabs(h * sw);
-    const double du = fma(rtol, fmax(fabs(u), fabs(u_new)), atol);
-    const double dw = fma(rtol, fmax(fabs(w), fabs(w_new)), atol);
-    const bool err_ok = (eu <= du) && (ew <= dw);
+    // |.| as operand modifiers of the compares and an integer mask of the
+    // high word (hiword(|x|) = hiword(x) & 0x7fffffff for every x), max by
+    // compare-select
+    const double eus = h * su, ews = h * sw;
+    const double du = fma(rtol, dmax(fabs(u), fabs(u_new)), atol);
+    const double dw = fma(rtol, dmax(fabs(w), fabs(w_new)), atol);
+    const bool err_ok = (fabs(eus) <= du) && (fabs(ews) <= dw);
     const bool geo_ok = u_new >= 0.5 * u;
-    const int du_ = __double2hiint(eu) - __double2hiint(du);
-    const int dw_ = __double2hiint(ew) - __double2hiint(dw);
+    const int du_ = (__double2hiint(eus) & 0x7fffffff) - __double2hiint(du);
+    const int dw_ = (__double2hiint(ews) & 0x7fffffff) - __double2hiint(dw);
     int q = (du_ > dw_ ? du_ : dw_) >> 18;
     q = q < kQMin ? kQMin : (q > kQMin + kQN - 1 ? kQMin + kQN - 1 : q);
     BHRT_ASSERT(q - kQMin >= 0 && q - kQMin < kQN);
     if (err_ok && geo_ok) {
         un = u_new;
         wn = w_new;
-        hn = fmin(h * grow[q - kQMin], hmax);
+        hn = dmin(h * grow[q - kQMin], hmax);
         return true;
     }
     hn = err_ok ? 0.5 * h : h * shrink[q - kQMin];
