@@ -195,6 +195,7 @@ def measure_secondary(device: int, peak: float, reps: int = 3, rank: int = 0, wo
             ctx.render_async(buf.data_ptr(), stream=st.cuda_stream)
             e1.record(st)
             ctx.finish()
+            e1.synchronize()  # finish() waits for the render only; the end event may trail it
             ms = e0.elapsed_time(e1)
             if r > 0 and (best is None or ms < best):
                 best = ms
@@ -288,6 +289,7 @@ def measure_secondary(device: int, peak: float, reps: int = 3, rank: int = 0, wo
             ctx.render_async(buf.data_ptr(), 0, sb2.s.height, 1, world, rank, stream=st.cuda_stream)
             e1.record(st)
             ctx.finish()
+            e1.synchronize()  # finish() waits for the render only; the end event may trail it
             ms = e0.elapsed_time(e1)
             if r > 0 and (best is None or ms < best):
                 best = ms
@@ -330,6 +332,7 @@ def measure_secondary(device: int, peak: float, reps: int = 3, rank: int = 0, wo
     ctx.render_async(buf.data_ptr(), stream=st.cuda_stream)
     e1.record(st)
     ctx.finish()
+    e1.synchronize()  # finish() waits for the render only; the end event may trail it
     ms = e0.elapsed_time(e1)
     rays = proj.s.width * proj.s.height * proj.s.spp
     stR = ctx.stats()

@@ -23,6 +23,7 @@ def timeit(sb, reps=3):
         e1.record(st)
         ctx.finish()
         if r:
+            e1.synchronize()  # finish() waits for the render only; the end event may trail it
             best = min(best, e0.elapsed_time(e1))
     s = ctx.stats()
     ctx.close()

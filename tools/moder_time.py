@@ -21,6 +21,7 @@ for r in range(reps + 1):
     ctx.render_async(buf.data_ptr(), stream=st.cuda_stream)
     e1.record(st)
     ctx.finish()
+    e1.synchronize()  # finish() waits for the render only; the end event may trail it
     ms = e0.elapsed_time(e1)
     s = ctx.stats()
     print(f"modeR {w}x{h}x{spp} rep {r}: {ms:.2f} ms  {s['rays'] / ms / 1e3:.2f} Mrays/s  "

@@ -25,4 +25,5 @@ for i in range(2):
     ctx.render_async(out.data_ptr(), stream=st.cuda_stream)
     e1.record(st)
     ctx.finish()
+    e1.synchronize()  # finish() waits for the render only; the end event may trail it
     print(f"frame {i}: {e0.elapsed_time(e1):.3f} ms", ctx.stats())

@@ -25,6 +25,7 @@ def main():
         ctx.render_async(out.data_ptr(), stream=st.cuda_stream)
         e1.record(st)
         ctx.finish()
+        e1.synchronize()  # finish() waits for the render only; the end event may trail it
         ms = e0.elapsed_time(e1)
         s = ctx.stats()
         rays = s["rays"]
