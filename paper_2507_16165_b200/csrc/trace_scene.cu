@@ -408,37 +408,16 @@ __device__ BHRT_INL_EVT bool step_events(const KParams& p, SM& sm, int t, double
     }
     if (ang) {
         // Conservative radial extent of the step's polyline. Its vertices lie
-        // on the Hermite interpolant u(t), t in [0, 1], whose range is spanned
-        // by the end values and the interior roots of u'(t) (fp32, widened by
-        // 1e-5 of the coefficient scale). A sub-chord of angle dl between
-        // radii r1, r2 stays within [min(r1, r2) cos(dl), max(r1, r2)].
+        // on the Hermite interpolant u(t), t in [0, 1]; u(t) minus the chord
+        // between its end values is -t(1-t)(a2 + a3(1+t)), at most
+        // (|a2| + 2|a3|)/4 in size (fp32, widened by 1e-5 of the coefficient
+        // scale). A sub-chord of angle dl between radii r1, r2 stays within
+        // [min(r1, r2) cos(dl), max(r1, r2)].
         float slo = 0.0f, shi = CUDART_INF_F;
         {
             const float a1 = (float)cu.a1, a2 = (float)cu.a2, a3 = (float)cu.a3, a0 = (float)ua;
-            float umin = fminf(a0, (float)ub), umax = fmaxf(a0, (float)ub);
-            const float A = 3.0f * a3, B = 2.0f * a2;
-            const float disc = B * B - 4.0f * A * a1;
-            if (disc >= 0.0f && A != 0.0f) {
-                const float sq = sqrtf(disc);
-                const float ta = (-B - sq) / (2.0f * A), tb = (-B + sq) / (2.0f * A);
-                if (ta > 0.0f && ta < 1.0f) {
-                    const float v = fmaf(fmaf(fmaf(a3, ta, a2), ta, a1), ta, a0);
-                    umin = fminf(umin, v);
-                    umax = fmaxf(umax, v);
-                }
-                if (tb > 0.0f && tb < 1.0f) {
-                    const float v = fmaf(fmaf(fmaf(a3, tb, a2), tb, a1), tb, a0);
-                    umin = fminf(umin, v);
-                    umax = fmaxf(umax, v);
-                }
-            } else if (A == 0.0f && B != 0.0f) {
-                const float ta = -a1 / B;
-                if (ta > 0.0f && ta < 1.0f) {
-                    const float v = fmaf(fmaf(a2, ta, a1), ta, a0);
-                    umin = fminf(umin, v);
-                    umax = fmaxf(umax, v);
-                }
-            }
+            const float dev = 0.25f * (fabsf(a2) + 2.0f * fabsf(a3));
+            float umin = fminf(a0, (float)ub) - dev, umax = fmaxf(a0, (float)ub) + dev;
             const float slack = 1e-5f * (fabsf(a0) + fabsf(a1) + fabsf(a2) + fabsf(a3));
             umin -= slack;
             umax += slack;
