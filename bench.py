@@ -230,12 +230,15 @@ def measure_secondary(device: int, peak: float, reps: int = 3, rank: int = 0, wo
         ctx.render_async(buf.data_ptr(), stream=st.cuda_stream)
         ctx.finish()
     scs = [scenes.config(4, frame=f) for f in range(frames)]
-    # two contexts in turn: frame f+1's scene upload (cull table on the host,
-    # async copies) proceeds while frame f renders; frames stay in order on
-    # one stream and each finish() waits for its own frame only
-    ctx2 = render.Context(device)
-    bufs = [buf, torch.empty_like(buf)]
-    ctxs = [ctx, ctx2]
+    # three contexts on three streams in turn: frame f+1's scene upload (cull
+    # table on the host, async copies) proceeds while frame f renders, and
+    # frame f+1's kernel fills the SMs while frame f's longest blocks drain
+    # (1/2/3 streams: 426/460/472 frames/s, tools/orbit_time.py); each
+    # finish() waits for its own frame only
+    NC = 3
+    ctxs = [ctx] + [render.Context(device) for _ in range(NC - 1)]
+    bufs = [buf] + [torch.empty_like(buf) for _ in range(NC - 1)]
+    strs = [st] + [torch.cuda.Stream(device) for _ in range(NC - 1)]
     mine = scs[rank::world]  # frame sharding f mod N (BASELINE.json config 4)
     torch.cuda.synchronize()
     if world > 1:
@@ -243,15 +246,16 @@ def measure_secondary(device: int, peak: float, reps: int = 3, rank: int = 0, wo
     t0 = time.perf_counter()
     flops4 = 0.0
     for f, sb in enumerate(mine):
-        c = ctxs[f % 2]
+        c = ctxs[f % NC]
         c.set_scene(sb)
-        c.render_async(bufs[f % 2].data_ptr(), stream=st.cuda_stream)
-        if f > 0:
-            ctxs[(f - 1) % 2].finish()
-            flops4 += roofline.launch_flops(mine[f - 1], ctxs[(f - 1) % 2].stats())
-    if mine:
-        ctxs[(len(mine) - 1) % 2].finish()
-        flops4 += roofline.launch_flops(mine[-1], ctxs[(len(mine) - 1) % 2].stats())
+        c.render_async(bufs[f % NC].data_ptr(), stream=strs[f % NC].cuda_stream)
+        if f >= NC - 1:
+            g = f - NC + 1
+            ctxs[g % NC].finish()
+            flops4 += roofline.launch_flops(mine[g], ctxs[g % NC].stats())
+    for g in range(max(0, len(mine) - NC + 1), len(mine)):
+        ctxs[g % NC].finish()
+        flops4 += roofline.launch_flops(mine[g], ctxs[g % NC].stats())
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
     tdt = torch.tensor([dt, flops4], device="cuda", dtype=torch.float64)
@@ -260,7 +264,8 @@ def measure_secondary(device: int, peak: float, reps: int = 3, rank: int = 0, wo
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
         dist.all_reduce(tdt, op=dist.ReduceOp.SUM)
         dt, flops4 = float(tmax.item()), float(tdt[1].item())
-    ctx2.close()
+    for c in ctxs[1:]:
+        c.close()
     out["config4"] = {"frames": frames, "seconds": dt, "frames/s": frames / dt,
                       "Mrays/s": frames * sb0.s.width * sb0.s.height * sb0.s.spp / dt / 1e6,
                       "size": [sb0.s.width, sb0.s.height, sb0.s.spp], "n_gpus": world,
