@@ -27,6 +27,7 @@ void launch_trace_polylines(const KParams& p, const double* rays, long long n, b
                             double* pts, int cap, int* npoly, cudaStream_t st);
 void launch_trace_rays(const KParams& p, const double* rays, long long n, bhrt_ray_record* records,
                        double* defl, cudaStream_t st);
+void launch_cull_build(const KParams& p, CullList* out, cudaStream_t st);
 
 namespace {
 
@@ -112,15 +113,14 @@ void factor_tables(double* grow, double* shrink) {
     }
 }
 
-// Conservative sphere masks per orbital-plane angle bin (KParams::cull).
-// A plane through the camera-hole axis v with unit normal
-// n(theta) = cos(theta) a + sin(theta) b cuts sphere (c, r) iff
-// |ca cos(theta) + cb sin(theta)| < r, i.e. theta within asin(r / rho) of
-// atan2(cb, ca) + pi/2 (mod pi), rho = |(ca, cb)|. Each interval is widened
-// by two bins before marking. Returns false when culling is not applicable.
+// Plane-angle culling basis (KParams::cull_a/b): every orbital plane of the
+// frame contains the camera-hole axis v, so its normal is
+// s (cos t a + sin t b) for unit a, b perpendicular to v. The per-bin
+// candidate lists themselves are built on the device (trace_scene.cu
+// build_cull_lists_kernel). Returns false when culling is not applicable.
 constexpr int kCullBins = 4096;
 
-bool build_cull_table(const bhrt_scene* s, KParams& k, std::vector<unsigned long long>& table) {
+bool cull_basis(const bhrt_scene* s, KParams& k) {
     if (s->integrator != BHRT_INTEGRATOR_RK4 && s->integrator != BHRT_INTEGRATOR_RKF45) return false;
     const HV3 v = hsub(hv(s->cam_pos), hv(s->center));
     if (hnorm(v) == 0.0) return false;
@@ -131,33 +131,9 @@ bool build_cull_table(const bhrt_scene* s, KParams& k, std::vector<unsigned long
     else if (std::fabs(vh.z) < std::fabs(vh.x)) axis = {0.0, 0.0, 1.0};
     const HV3 a = hnormalized(hcross(vh, axis));
     const HV3 b = hcross(vh, a);
-    const int words = (s->n_spheres + 63) / 64;
-    table.assign(static_cast<size_t>(kCullBins) * words, 0ull);
-    const double bw = kPi / kCullBins;
-    for (int i = 0; i < s->n_spheres; ++i) {
-        const HV3 c = hsub(hv(s->spheres[i].center), hv(s->center));
-        const double ca = hdot(c, a), cb = hdot(c, b);
-        const double rho = std::hypot(ca, cb);
-        const double r = s->spheres[i].radius;
-        const unsigned long long bit = 1ull << (i % 64);
-        const int w = i / 64;
-        if (rho <= r * (1.0 + 1e-9) + 1e-12) {
-            for (int j = 0; j < kCullBins; ++j) table[static_cast<size_t>(j) * words + w] |= bit;
-            continue;
-        }
-        const double half = std::asin(r / rho);
-        const double mid = std::atan2(cb, ca) + 0.5 * kPi;
-        const long lo = static_cast<long>(std::floor((mid - half) / bw)) - 2;
-        const long hi = static_cast<long>(std::floor((mid + half) / bw)) + 2;
-        for (long j = lo; j <= hi; ++j) {
-            const long jj = ((j % kCullBins) + kCullBins) % kCullBins;
-            table[static_cast<size_t>(jj) * words + w] |= bit;
-        }
-    }
     hput(k.cull_a, a);
     hput(k.cull_b, b);
     k.cull_bins = kCullBins;
-    k.cull_words = words;
     return true;
 }
 
@@ -213,8 +189,7 @@ struct bhrt_ctx {
     DevBuf<double> checker;     // checker cell boundaries (KParams::checker_tab)
     DevBuf<uint8_t> out;
     DevBuf<unsigned long long> stats;
-    DevBuf<unsigned long long> cull;
-    DevBuf<float> sph_frame;  // KParams::sph_frame
+    DevBuf<CullList> cull;  // KParams::cull, 2 * kCullBins lists
     DevBuf<double> tab_smp, tab_ends, tab_psi0;
     DevBuf<int32_t> tab_kind, tab_n;
     bool has_table = false;
@@ -445,7 +420,6 @@ void bhrt_ctx_destroy(bhrt_ctx* c) {
     c->out.release();
     c->stats.release();
     c->cull.release();
-    c->sph_frame.release();
     c->checker.release();
     c->rays.release();
     c->defl.release();
@@ -555,25 +529,9 @@ int bhrt_ctx_set_scene(bhrt_ctx* c, const bhrt_scene* s, bhrt_status_info* info)
     // host data -> pinned staging -> device (async on the upload stream)
     const size_t sky_bytes = s->sky_kind == BHRT_SKY_IMAGE ? 3ull * s->sky_width * s->sky_height : 0;
     const size_t sph_bytes = sizeof(bhrt_sphere) * static_cast<size_t>(s->n_spheres);
-    std::vector<unsigned long long> table;
-    const bool cull = s->n_spheres > 0 && build_cull_table(s, k, table);
-    const size_t cull_bytes = cull ? sizeof(unsigned long long) * table.size() : 0;
-    std::vector<float> sfr;  // KParams::sph_frame
-    if (cull) {
-        const HV3 a = hv(k.cull_a), b = hv(k.cull_b), e1 = hv(k.cam_e1);
-        for (int i = 0; i < s->n_spheres; ++i) {
-            const HV3 cc = hsub(hv(s->spheres[i].center), hv(s->center));
-            const double r = s->spheres[i].radius;
-            sfr.push_back(static_cast<float>(hdot(cc, a)));
-            sfr.push_back(static_cast<float>(hdot(cc, b)));
-            sfr.push_back(static_cast<float>(hdot(cc, e1)));
-            // fp32 slack: the device forms c.n, c.e2 from rounded floats
-            sfr.push_back(static_cast<float>(r + 1e-5 * (hnorm(cc) + r) + 1e-6));
-        }
-    }
-    const size_t sfr_bytes = sizeof(float) * sfr.size();
+    const bool cull = s->n_spheres > 0 && cull_basis(s, k);
     const size_t chk_bytes = sizeof checker;
-    const size_t need = chk_bytes + sky_bytes + sph_bytes + cull_bytes + sfr_bytes;
+    const size_t need = chk_bytes + sky_bytes + sph_bytes;
     c->upload_bytes = need;
     if (need > c->staging_cap) {
         if (c->staging) CK(cudaFreeHost(c->staging));
@@ -603,17 +561,12 @@ int bhrt_ctx_set_scene(bhrt_ctx* c, const bhrt_scene* s, bhrt_status_info* info)
         CK(cudaMemcpyAsync(c->spheres.p, c->staging + off, sph_bytes, cudaMemcpyHostToDevice, c->up_stream));
         off += sph_bytes;
         k.spheres = c->spheres.p;
-        if (cull) {
-            if (c->cull.ensure(table.size())) return set_info(info, BHRT_DEVICE, -1, -1, "cull alloc failed");
-            std::memcpy(c->staging + off, table.data(), cull_bytes);
-            CK(cudaMemcpyAsync(c->cull.p, c->staging + off, cull_bytes, cudaMemcpyHostToDevice, c->up_stream));
-            off += cull_bytes;
+        if (cull) {  // the candidate lists, from the spheres just uploaded
+            if (c->cull.ensure(2 * static_cast<size_t>(kCullBins)))
+                return set_info(info, BHRT_DEVICE, -1, -1, "cull alloc failed");
             k.cull = c->cull.p;
-            if (c->sph_frame.ensure(sfr.size())) return set_info(info, BHRT_DEVICE, -1, -1, "sphere alloc failed");
-            std::memcpy(c->staging + off, sfr.data(), sfr_bytes);
-            CK(cudaMemcpyAsync(c->sph_frame.p, c->staging + off, sfr_bytes, cudaMemcpyHostToDevice, c->up_stream));
-            off += sfr_bytes;
-            k.sph_frame = c->sph_frame.p;
+            launch_cull_build(k, c->cull.p, c->up_stream);
+            CK(cudaGetLastError());
         }
     }
     k.fused_shade = (32 % s->spp) == 0 ? 1 : 0;

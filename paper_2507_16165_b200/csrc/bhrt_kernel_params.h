@@ -10,6 +10,16 @@
 
 namespace bhrt_b200 {
 
+constexpr int kCullSlots = 8;  // candidate spheres kept per ray (more: test all)
+
+// Candidate spheres of one (plane-angle bin, orientation): 144 bytes.
+struct alignas(16) CullList {
+    int32_t n;                  // candidates (<= kCullSlots); -1: more, test every sphere
+    float next_lo;              // smallest window start
+    uint8_t k[kCullSlots];      // sphere indices, increasing
+    float win[kCullSlots][4];   // (lo, hi) unwrapped window angle, (rlo, rhi) radial extent
+};
+
 constexpr int kQMin = -64;  // RKF45 controller table range
 constexpr int kQN = 96;
 // Largest q with grow factor 0.9 * 2^(-(q+1)/20) >= 1 (checked against the
@@ -69,19 +79,16 @@ struct KParams {
     const double* grow;
     const double* shrink;
     // Sphere culling by orbital-plane angle. Every orbital plane contains the
-    // camera-hole axis v, so planes form a pencil n(theta) = cos(theta) a +
-    // sin(theta) b (a, b unit, perpendicular to v). cull[bin * cull_words + w]
-    // is a CONSERVATIVE mask of the spheres a plane with theta in the bin can
-    // cut; the exact fp64 test |c.n| < r still decides.
-    const unsigned long long* cull;
-    int32_t cull_bins, cull_words;
+    // camera-hole axis v, so planes form a pencil n = s (cos t a + sin t b)
+    // (a, b unit, perpendicular to v; s = +-1 the orientation). cull points
+    // at 2 * cull_bins CullList records, [2 bin + (s < 0)], built on the
+    // device per frame (build_cull_lists_kernel): the CONSERVATIVE candidate
+    // spheres of every plane in the bin with their angular windows and
+    // radial extents; the exact fp64 tests still decide.
+    const void* cull;
+    int32_t cull_bins;
+    int32_t pad2;
     double cull_a[3], cull_b[3];
-    // per-frame sphere records for the candidate prefilter, 4 floats per
-    // sphere: (c.a, c.b, c.e1, r + slack), c = centre - hole, a/b = cull_a/b,
-    // e1 = cam_e1. Every orbital plane n(theta) = cos(theta) b - sin(theta) a
-    // contains e1, so c.n and c.e2 are two fp32 fmas per sphere (conservative:
-    // the exact fp64 tests run in sphere_search)
-    const float* sph_frame;
     // 1: shade inside the trace kernel (spp divides 32; the spp samples of a
     // pixel are adjacent lanes, summed in sample order by warp shuffles)
     int32_t fused_shade;

@@ -352,8 +352,14 @@ __global__ void __launch_bounds__(128, BHRT_TAB_MINB) trace_table_kernel(const _
                     while (next_disk < stop) {
                         const double ph = next_disk;
                         double ui = -1.0, uj = -1.0;
+#ifdef BHRT_EXPERIMENT_NOTABU
+                        // timing experiment only: no orbit-sample gathers
+                        if (wi > 0.0) ui = 0.01 * (1.0 + ph);
+                        if (wj > 0.0) uj = 0.01 * (1.0 + ph);
+#else
                         if (wi > 0.0) ui = table_u(T, ie, p0i + sgn * ph);
                         if (wj > 0.0) uj = table_u(T, ie + 1, p0j + sgn * ph);
+#endif
                         nevals += (wi > 0.0) + (wj > 0.0);
                         double u_ev;
                         if (wi > 0.0 && wj > 0.0 && ui >= 0.0 && uj >= 0.0)

@@ -26,7 +26,7 @@ namespace bhrt_b200 {
 #define BHRT_SCENE_BLOCK 128
 #endif
 constexpr int kBlock = BHRT_SCENE_BLOCK;
-constexpr int kSlots = 8;
+constexpr int kSlots = kCullSlots;
 constexpr int kSphSm = 128;          // spheres staged in shared memory
 constexpr float kWinMargin = 5e-4f;  // fp32 window slack (rad); windows only cull
 #ifndef BHRT_SCENE_MINB
@@ -81,26 +81,6 @@ __device__ __forceinline__ float atan2_cull(float y, float x) {
     if (ay > ax) r = 1.57079637f - r;
     if (x < 0.0f) r = 3.14159274f - r;
     return copysignf(r, y);
-}
-
-// The same window from fp32 inputs (the cull-table path): origin outside the
-// circle iff rc > rho (rho carries the record's slack, so a near-boundary
-// case falls to the infinite window).
-__device__ __forceinline__ void sphere_window_ff(float cx, float cy, float rcf, float rhof, float& lo, float& hi) {
-    if (!(rcf > rhof)) {
-        lo = -CUDART_INF_F;
-        hi = CUDART_INF_F;
-        return;
-    }
-    const float x = __fdividef(rhof, rcf);
-    const float a = x <= 0.5f ? x * (1.0f + 0.2f * x * x) * 1.0001f : 1.5708f;
-    const float pc = atan2_cull(cy, cx);
-    lo = pc - a - kWinMargin;
-    hi = pc + a + kWinMargin;
-    if (hi < 0.0f) {
-        lo += 2.0f * (float)PI_D;
-        hi += 2.0f * (float)PI_D;
-    }
 }
 
 // rcf = |(cx, cy)| and rhof = sqrt(rho2) in fp32 (shared with the radial extent)
@@ -178,49 +158,30 @@ __device__ BHRT_INL_SETUP double events_setup(const KParams& p, SM& sm, int t, V
     const int ns = p.n_spheres;
 #endif
     if (p.cull && ns > 0) {
-        // plane-angle bin -> conservative sphere mask (host table, KParams::cull)
+        // plane-angle bin and orientation -> the frame's precomputed list of
+        // conservative candidates with their windows (KParams::cull,
+        // build_cull_lists_kernel): a 144-byte record copied to the ray's slots
         const float na = (float)(n.x * p.cull_a[0] + n.y * p.cull_a[1] + n.z * p.cull_a[2]);
         const float nb = (float)(n.x * p.cull_b[0] + n.y * p.cull_b[1] + n.z * p.cull_b[2]);
-        float th = atan2_cull(nb, na);  // the table is padded by 2 bins (1.5e-3 rad)
-        if (th < 0.0f) th += (float)PI_D;
+        float th = atan2_cull(nb, na);  // lists cover +-1e-5 rad beyond their bin
+        const bool flip = th < 0.0f;
+        if (flip) th += (float)PI_D;
         int bin = (int)(th * (float)(p.cull_bins / PI_D));
         bin = bin < 0 ? 0 : (bin >= p.cull_bins ? p.cull_bins - 1 : bin);
-        const unsigned long long* row = p.cull + (size_t)bin * p.cull_words;
-        // Candidates in fp32 from the per-frame records (KParams::sph_frame):
-        // n = cos(t) b - sin(t) a and e2 = cos(t) a + sin(t) b with
-        // (cos t, sin t) = (n.b, -n.a), so c.n = na ca + nb cb and
-        // c.e2 = nb ca - na cb. A CONSERVATIVE superset of the oracle's exact
-        // |c.n| < r set (slack in the record's radius); sphere_search re-runs
-        // the exact fp64 test and the windows only cull, so results are the
-        // oracle's. Replaces four fp64 loads + two fp64 dots per sphere.
-        const float4* sf = reinterpret_cast<const float4*>(p.sph_frame);
-        bool go = true;
-        for (int w = 0; w < p.cull_words && go; ++w) {
-            unsigned long long m = __ldg(row + w);
-            while (m && go) {
-                const int k = w * 64 + __ffsll((long long)m) - 1;
-                m &= m - 1;
-                const float4 f = __ldg(sf + k);  // (ca, cb, cx, r + slack)
-                const float dn = fmaf(na, f.x, nb * f.y);
-                if (!(fabsf(dn) < f.w)) continue;
-                if (nc == kSlots) {
-                    nc = -1;
-                    go = false;
-                    break;
-                }
-                const float cx = f.z, cy = fmaf(nb, f.x, -na * f.y);
-                const float rho2 = fmaxf(fmaf(f.w, f.w, -dn * dn), 0.0f);  // >= r^2 - dn^2 (slack)
-                const float rc = sqrtf(fmaf(cx, cx, cy * cy)), rho = sqrtf(rho2);
-                float lo, hi;
-                sphere_window_ff(cx, cy, rc, rho, lo, hi);
-                sm.lo[nc][t] = lo;
-                sm.hi[nc][t] = hi;
-                sm.rlo[nc][t] = (rc - rho) - 1e-5f * (rc + rho);
-                sm.rhi[nc][t] = (rc + rho) * (1.0f + 1e-5f);
-                BHRT_ASSERT(k >= 0 && k < p.n_spheres && nc >= 0 && nc < kSlots);
-                sm.k[nc][t] = (unsigned char)k;
-                next_sph = fminf(next_sph, lo);
-                ++nc;
+        const CullList* L = static_cast<const CullList*>(p.cull) + (2 * bin + (flip ? 1 : 0));
+        const int2 hdr = __ldg(reinterpret_cast<const int2*>(L));
+        nc = hdr.x;
+        if (nc > 0) {
+            next_sph = __int_as_float(hdr.y);
+            const uint2 kk = __ldg(reinterpret_cast<const uint2*>(L->k));
+            const float4* W = reinterpret_cast<const float4*>(L->win);
+            for (int i = 0; i < nc; ++i) {
+                const float4 w = __ldg(W + i);
+                sm.lo[i][t] = w.x;
+                sm.hi[i][t] = w.y;
+                sm.rlo[i][t] = w.z;
+                sm.rhi[i][t] = w.w;
+                sm.k[i][t] = (unsigned char)((i < 4 ? kk.x : kk.y) >> (8 * (i & 3)));
             }
         }
     } else {
@@ -751,6 +712,98 @@ __global__ void __launch_bounds__(kBlock, BHRT_SCENE_MINB) trace_scene_kernel(co
     }
     finish_sample(p, valid, id, H.obj, H.sphere, H.point, phi, nsteps, nrej);
     warp_add_stats(p.stats, nsteps, nrej, valid ? 1u : 0u);
+}
+
+// ----------------------------------------------------------------- culling lists
+// One thread per (plane-angle bin, orientation): the conservative candidate
+// list of EVERY orbital plane of the frame whose normal is
+// s (cos t a + sin t b) with t in the bin widened by kCullEps (the ray's
+// fp32 angle is within 3e-6 of its exact one) and s = +1 / -1. With
+// f(t) = ca cos t + cb sin t and g(t) = ca sin t - cb cos t (c = centre - hole,
+// ca = c.a, cb = c.b, cx = c.e1): c.n = s f, c.e2 = s g, and g is monotone on
+// the bin unless f changes sign there (then g reaches +-|(ca, cb)|). A sphere
+// is a candidate when min |f| < r; its window is the union over the bin of
+// [atan2(cy, cx) -+ asin(rho / rc)] (rho <= sqrt(r^2 - min f^2), rc >= its
+// minimum), infinite when the circle may contain the hole or straddle the
+// atan2 cut; its radial extent [min rc - rho, max rc + rho]. All in double
+// with relative slack, then rounded outward — culling only selects which
+// exact fp64 tests run (sphere_search), so the lists cannot change results.
+constexpr double kCullEps = 1e-5;
+constexpr double kCullMargin = 1e-4;  // rad, beyond the exact union (fp32 rounding of the windows)
+
+__global__ void __launch_bounds__(128) build_cull_lists_kernel(const __grid_constant__ KParams p, CullList* out) {
+    const int id = blockIdx.x * blockDim.x + threadIdx.x;
+    if (id >= 2 * p.cull_bins) return;
+    const int bin = id >> 1;
+    const double sg = (id & 1) ? -1.0 : 1.0;
+    const double bw = PI_D / p.cull_bins;
+    double s0, c0, s1, c1;
+    sincos(bin * bw - kCullEps, &s0, &c0);
+    sincos((bin + 1) * bw + kCullEps, &s1, &c1);
+    const V3 a = vld(p.cull_a), b = vld(p.cull_b), e1 = vld(p.cam_e1), O = vld(p.center);
+    CullList L;
+    L.n = 0;
+    float next = CUDART_INF_F;
+#pragma unroll
+    for (int i = 0; i < kCullSlots; ++i) {
+        L.k[i] = 0;
+        L.win[i][0] = L.win[i][1] = L.win[i][2] = L.win[i][3] = 0.0f;
+    }
+    for (int k = 0; k < p.n_spheres; ++k) {
+        const V3 c = sub(vld(p.spheres[k].center), O);
+        const double r = p.spheres[k].radius;
+        const double ca = dot(c, a), cb = dot(c, b), cx = dot(c, e1);
+        const double f0 = ca * c0 + cb * s0, f1 = ca * c1 + cb * s1;
+        const double g0 = ca * s0 - cb * c0, g1 = ca * s1 - cb * c1;
+        const double R = sqrt(ca * ca + cb * cb);
+        const double slack = 1e-9 * (R + fabs(cx) + r) + 1e-12;
+        const bool fcross = !(f0 > 0.0 && f1 > 0.0) && !(f0 < 0.0 && f1 < 0.0);
+        const double fmn = fcross ? 0.0 : fmin(fabs(f0), fabs(f1));
+        if (!(fmn < r + slack)) continue;  // no plane of the bin cuts the sphere
+        if (L.n == kCullSlots) {
+            L.n = -1;  // more than the slots: the rays of this list test every sphere
+            break;
+        }
+        const double fl = fmn > slack ? fmn - slack : 0.0;
+        const double rho = sqrt(fmax(r * r - fl * fl, 0.0)) * (1.0 + 1e-9) + slack;
+        double glo = fmin(g0, g1), ghi = fmax(g0, g1);
+        if (fcross) {
+            if (g0 + g1 > 0.0) ghi = R; else glo = -R;
+        }
+        glo -= slack;
+        ghi += slack;
+        const double cylo = sg > 0.0 ? glo : -ghi, cyhi = sg > 0.0 ? ghi : -glo;
+        const bool cy0 = cylo <= 0.0 && cyhi >= 0.0;
+        const double cymin2 = cy0 ? 0.0 : fmin(cylo * cylo, cyhi * cyhi);
+        const double cymax2 = fmax(cylo * cylo, cyhi * cyhi);
+        const double rcmin = sqrt(cx * cx + cymin2), rcmax = sqrt(cx * cx + cymax2);
+        float lo = -CUDART_INF_F, hi = CUDART_INF_F;
+        if (rcmin > rho && !(cx < 0.0 && cy0)) {
+            const double half = asin(fmin(1.0, rho / rcmin));
+            const double pa = atan2(cylo, cx), pb = atan2(cyhi, cx);
+            double l = fmin(pa, pb) - half - kCullMargin, h = fmax(pa, pb) + half + kCullMargin;
+            if (h < 0.0) {
+                l += 2.0 * PI_D;
+                h += 2.0 * PI_D;
+            }
+            lo = (float)l;
+            hi = (float)h;
+        }
+        const int i = L.n++;
+        L.k[i] = (uint8_t)k;
+        L.win[i][0] = lo;
+        L.win[i][1] = hi;
+        L.win[i][2] = (float)((rcmin - rho) * (1.0 - 1e-6) - 1e-6);
+        L.win[i][3] = (float)((rcmax + rho) * (1.0 + 1e-6) + 1e-6);
+        next = fminf(next, lo);
+    }
+    L.next_lo = next;
+    out[id] = L;
+}
+
+void launch_cull_build(const KParams& p, CullList* out, cudaStream_t st) {
+    const int n = 2 * p.cull_bins;
+    build_cull_lists_kernel<<<(n + 127) / 128, 128, 0, st>>>(p, out);
 }
 
 void launch_scene(const KParams& p, cudaStream_t st) {
