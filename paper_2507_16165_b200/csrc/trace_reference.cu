@@ -15,7 +15,65 @@
 namespace bhrt_b200 {
 
 // ================================================================= mode R
-// Dormand-Prince 5(4) tableau (geodesic.cpp:89-100), same constant expressions.
+// Dormand-Prince 5(4) tableau (geodesic.cpp:89-100), same constant expressions,
+// in the constant bank: as literals every use was rematerialised by two UMOVs
+// inside the window loop (64 per step); DMUL takes a constant-bank operand.
+#ifndef BHRT_DOPRI_LITERALS
+static __constant__ double kDopri[26] = {
+    1.0 / 5.0,  // A21
+    3.0 / 40.0,  // A31
+    9.0 / 40.0,  // A32
+    44.0 / 45.0,  // A41
+    -56.0 / 15.0,  // A42
+    32.0 / 9.0,  // A43
+    19372.0 / 6561.0,  // A51
+    -25360.0 / 2187.0,  // A52
+    64448.0 / 6561.0,  // A53
+    -212.0 / 729.0,  // A54
+    9017.0 / 3168.0,  // A61
+    -355.0 / 33.0,  // A62
+    46732.0 / 5247.0,  // A63
+    49.0 / 176.0,  // A64
+    -5103.0 / 18656.0,  // A65
+    35.0 / 384.0,  // B1
+    500.0 / 1113.0,  // B3
+    125.0 / 192.0,  // B4
+    -2187.0 / 6784.0,  // B5
+    11.0 / 84.0,  // B6
+    71.0 / 57600.0,  // E1
+    -71.0 / 16695.0,  // E3
+    71.0 / 1920.0,  // E4
+    -17253.0 / 339200.0,  // E5
+    22.0 / 525.0,  // E6
+    -1.0 / 40.0,  // E7
+};
+#define A21 (kDopri[0])
+#define A31 (kDopri[1])
+#define A32 (kDopri[2])
+#define A41 (kDopri[3])
+#define A42 (kDopri[4])
+#define A43 (kDopri[5])
+#define A51 (kDopri[6])
+#define A52 (kDopri[7])
+#define A53 (kDopri[8])
+#define A54 (kDopri[9])
+#define A61 (kDopri[10])
+#define A62 (kDopri[11])
+#define A63 (kDopri[12])
+#define A64 (kDopri[13])
+#define A65 (kDopri[14])
+#define B1 (kDopri[15])
+#define B3 (kDopri[16])
+#define B4 (kDopri[17])
+#define B5 (kDopri[18])
+#define B6 (kDopri[19])
+#define E1 (kDopri[20])
+#define E3 (kDopri[21])
+#define E4 (kDopri[22])
+#define E5 (kDopri[23])
+#define E6 (kDopri[24])
+#define E7 (kDopri[25])
+#else
 #define A21 (1.0 / 5.0)
 #define A31 (3.0 / 40.0)
 #define A32 (9.0 / 40.0)
@@ -42,6 +100,7 @@ namespace bhrt_b200 {
 #define E5 (-17253.0 / 339200.0)
 #define E6 (22.0 / 525.0)
 #define E7 (-1.0 / 40.0)
+#endif
 
 __device__ __forceinline__ double rhs_w(double u, double mass) { return 3.0 * mass * u * u - u; }
 
