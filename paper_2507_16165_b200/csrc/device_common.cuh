@@ -200,21 +200,35 @@ __device__ __forceinline__ void initial_conditions(const KParams& p, V3 dir, dou
 // Horner), then the octant fix-up with two-part pi/2, pi. Normative op order
 // (oracle/bhrt_oracle.c atan2_est = device_common.cuh atan2_est). Finite
 // arguments, not both zero.
+// atan2_est's Chebyshev coefficients in the constant bank (as literals each
+// costs two UMOV/IMAD per use); pairs (odd, even) of the Estrin first level.
+static __constant__ double kAtanC[20] = {
+    0x1.9999999999620p-3, -0x1.5555555555555p-2,
+    0x1.c71c71bb00a6cp-4, -0x1.24924924753ecp-3,
+    0x1.3b1399d1dcdc7p-4, -0x1.745d15ee35819p-4,
+    0x1.e1d0239d392a6p-5, -0x1.110fff599e4d2p-4,
+    0x1.841dcf603a209p-5, -0x1.aebbb1647a168p-5,
+    0x1.3328700bb8169p-5, -0x1.5d02278205cc7p-5,
+    0x1.843f4bca23369p-6, -0x1.00390504e9f2fp-5,
+    0x1.123baedb61abdp-7, -0x1.fd0e4de8fed90p-7,
+    0x1.1325b2f8964bep-10, -0x1.ca3677db66678p-9,
+    0x1.2f07811f9f6e9p-16, -0x1.a359b96a4eee4p-13,
+};
 __device__ __forceinline__ double atan2_est(double y, double x) {
     const double ax = fabs(x), ay = fabs(y);
     const double mx = ax < ay ? ay : ax, mn = ax < ay ? ax : ay;
     const double t = mn / mx;
     const double s = t * t, s2 = s * s, s4 = s2 * s2, s8 = s4 * s4, s16 = s8 * s8;
-    const double b0 = fma(0x1.9999999999620p-3, s, -0x1.5555555555555p-2);
-    const double b1 = fma(0x1.c71c71bb00a6cp-4, s, -0x1.24924924753ecp-3);
-    const double b2 = fma(0x1.3b1399d1dcdc7p-4, s, -0x1.745d15ee35819p-4);
-    const double b3 = fma(0x1.e1d0239d392a6p-5, s, -0x1.110fff599e4d2p-4);
-    const double b4 = fma(0x1.841dcf603a209p-5, s, -0x1.aebbb1647a168p-5);
-    const double b5 = fma(0x1.3328700bb8169p-5, s, -0x1.5d02278205cc7p-5);
-    const double b6 = fma(0x1.843f4bca23369p-6, s, -0x1.00390504e9f2fp-5);
-    const double b7 = fma(0x1.123baedb61abdp-7, s, -0x1.fd0e4de8fed90p-7);
-    const double b8 = fma(0x1.1325b2f8964bep-10, s, -0x1.ca3677db66678p-9);
-    const double b9 = fma(0x1.2f07811f9f6e9p-16, s, -0x1.a359b96a4eee4p-13);
+    const double b0 = fma(kAtanC[0], s, kAtanC[1]);
+    const double b1 = fma(kAtanC[2], s, kAtanC[3]);
+    const double b2 = fma(kAtanC[4], s, kAtanC[5]);
+    const double b3 = fma(kAtanC[6], s, kAtanC[7]);
+    const double b4 = fma(kAtanC[8], s, kAtanC[9]);
+    const double b5 = fma(kAtanC[10], s, kAtanC[11]);
+    const double b6 = fma(kAtanC[12], s, kAtanC[13]);
+    const double b7 = fma(kAtanC[14], s, kAtanC[15]);
+    const double b8 = fma(kAtanC[16], s, kAtanC[17]);
+    const double b9 = fma(kAtanC[18], s, kAtanC[19]);
     const double d0 = fma(b1, s2, b0);
     const double d1 = fma(b3, s2, b2);
     const double d2 = fma(b5, s2, b4);
