@@ -27,7 +27,6 @@ namespace bhrt_b200 {
 #endif
 constexpr int kBlock = BHRT_SCENE_BLOCK;
 constexpr int kSlots = kCullSlots;
-constexpr int kSphSm = 128;          // spheres staged in shared memory
 constexpr float kWinMargin = 5e-4f;  // fp32 window slack (rad); windows only cull
 #ifndef BHRT_SCENE_MINB
 // min resident blocks per SM (register cap 102): measured on B200, config 2:
@@ -40,7 +39,6 @@ constexpr float kWinMargin = 5e-4f;  // fp32 window slack (rad); windows only cu
 template <int NS>
 struct SceneSmT {
     static constexpr int kNS = NS;
-    float4 sph[kSphSm];  // (cx, cy, cz, r + fp32 slack) relative to the hole: cull prefilter
     double e2[3][NS], n[3][NS];  // e1 is the per-frame KParams::cam_e1
     double sigma[NS], energy[NS], next_disk[NS];
     float lo[kSlots][NS], hi[kSlots][NS];   // angular window (unwrapped phi)
@@ -83,30 +81,6 @@ __device__ __forceinline__ float atan2_cull(float y, float x) {
     return copysignf(r, y);
 }
 
-// rcf = |(cx, cy)| and rhof = sqrt(rho2) in fp32 (shared with the radial extent)
-__device__ __forceinline__ void sphere_window_f(double cx, double cy, double rho2, float rcf, float rhof,
-                                                float& lo, float& hi) {
-    const double q = cx * cx + cy * cy - rho2;  // rc^2 - rho^2
-    if (!(q > 0.0)) {
-        lo = -CUDART_INF_F;
-        hi = CUDART_INF_F;
-        return;
-    }
-    // half-width asin(x), x = rho/rc, bounded from above without a second
-    // atan2: asin(x) <= x (1 + x^2/5) on [0, 1/2] (series 1/6 + 3x^2/40 + ...),
-    // and <= pi/2 beyond.
-    const float x = __fdividef(rhof, rcf);  // culling only: ~2 ulp is far inside the margins
-    const float a = x <= 0.5f ? x * (1.0f + 0.2f * x * x) * 1.0001f : 1.5708f;
-    (void)q;
-    const float pc = atan2_cull((float)cy, (float)cx);
-    lo = pc - a - kWinMargin;
-    hi = pc + a + kWinMargin;
-    if (hi < 0.0f) {
-        lo += 2.0f * (float)PI_D;
-        hi += 2.0f * (float)PI_D;
-    }
-}
-
 // Disk line + sphere candidates (oracle ray_events_setup). Returns the first
 // event angle.
 template <class SM>
@@ -127,31 +101,6 @@ __device__ BHRT_INL_SETUP double events_setup(const KParams& p, SM& sm, int t, V
     sm.next_disk[t] = next_disk;
     int nc = 0;
     float next_sph = CUDART_INF_F;
-    // exact fp64 candidate test (oracle: |c.n| < r), in increasing sphere order
-    auto consider = [&](int k) -> bool {
-        const V3 c = sphere_c(p, k);
-        const double r = __ldg(&p.spheres[k].radius);
-        const double dn = dot(c, n);
-        if (!(fabs(dn) < r)) return true;
-        if (nc == kSlots) {
-            nc = -1;
-            return false;
-        }
-        const double cx = dot(c, e1), cy = dot(c, e2);
-        const double rho2 = r * r - dn * dn;
-        const float rc = sqrtf((float)(cx * cx + cy * cy)), rho = sqrtf((float)rho2);
-        float lo, hi;
-        sphere_window_f(cx, cy, rho2, rc, rho, lo, hi);
-        sm.lo[nc][t] = lo;
-        sm.hi[nc][t] = hi;
-        sm.rlo[nc][t] = (rc - rho) - 1e-5f * (rc + rho);  // fp32 rounding << 1e-5
-        sm.rhi[nc][t] = (rc + rho) * (1.0f + 1e-5f);
-        BHRT_ASSERT(k >= 0 && k < p.n_spheres && nc >= 0 && nc < kSlots);
-        sm.k[nc][t] = (unsigned char)k;
-        next_sph = fminf(next_sph, lo);
-        ++nc;
-        return true;
-    };
 #ifdef BHRT_EXPERIMENT_NOCAND
     const int ns = 0;  // timing experiment only: no sphere candidates
 #else
@@ -184,16 +133,8 @@ __device__ BHRT_INL_SETUP double events_setup(const KParams& p, SM& sm, int t, V
                 sm.k[i][t] = (unsigned char)((i < 4 ? kk.x : kk.y) >> (8 * (i & 3)));
             }
         }
-    } else {
-        const float nxf = (float)n.x, nyf = (float)n.y, nzf = (float)n.z;
-        for (int k = 0; k < ns; ++k) {
-            if (k < kSphSm) {  // conservative fp32 prefilter; the fp64 test decides
-                const float4 f = sm.sph[k];
-                const float dnf = f.x * nxf + f.y * nyf + f.z * nzf;
-                if (!(fabsf(dnf) < f.w)) continue;
-            }
-            if (!consider(k)) break;
-        }
+    } else if (ns > 0) {
+        nc = -1;  // no culling basis (never for a valid camera): every event step tests every sphere
     }
     if (nc < 0) next_sph = -CUDART_INF_F;
 #ifdef BHRT_EXPERIMENT_NOSPHEREEVENTS
@@ -531,14 +472,6 @@ template <int INTEG, bool DIAG>
 __global__ void __launch_bounds__(kBlock, BHRT_SCENE_MINB) trace_scene_kernel(const __grid_constant__ KParams p) {
     __shared__ SceneSm sm;
     const int t = threadIdx.x;
-    // the fp32 prefilter is read only without the plane-angle cull table
-    for (int k = t; !p.cull && k < p.n_spheres && k < kSphSm; k += blockDim.x) {
-        const V3 c = sphere_c(p, k);
-        const double r = p.spheres[k].radius;
-        const float slack = 1e-5f * (float)(norm(c) + r) + 1e-6f;
-        sm.sph[k] = make_float4((float)c.x, (float)c.y, (float)c.z, (float)r + slack);
-    }
-    if (!p.cull) __syncthreads();  // uniform over the grid (kernel parameter)
 
     const long long n = (long long)p.n_rows * p.width * p.spp;
     const long long i = (long long)blockIdx.x * blockDim.x + t;
