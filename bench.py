@@ -440,6 +440,46 @@ def dropin_e2e(scene, device: int, iters: int, flush) -> dict:
     return {"ms": ms, "image": out}
 
 
+def gpu_reference_harness(scene, device: int, repeats: int = 5) -> dict | None:
+    """The GPU timed by the reference's OWN harness: dropin/bhrt_bench_b200
+    (csrc/bench_main.cpp) runs bench.cpp's run_strong_scaling(scene, {1},
+    repeats) and emit_csv unchanged, its default RenderRunner render_image
+    resolving to render_shim.cpp (mode R, byte-identical to the reference).
+    Scene: the sky-only projection of the workload at full size — the same
+    scene reference_sky_only times on the CPU through the same harness. One
+    untimed warm-up frame first (CUDA context); mean of the run = -1 row."""
+    import subprocess
+    import tempfile
+
+    from paper_2507_16165_b200 import scenes
+    exe = os.path.join(ROOT, "paper_2507_16165_b200", "dropin", "bhrt_bench_b200")
+    if not os.path.exists(exe):
+        return None
+    proj = scenes.sky_only_projection(scene)
+    sky = proj.sky
+    with tempfile.TemporaryDirectory() as d:
+        cfg, bg, out = (os.path.join(d, n) for n in ("scene.txt", "sky.ppm", "bench.csv"))
+        open(cfg, "w").write(proj.to_text())
+        with open(bg, "wb") as f:
+            f.write(f"P6\n{sky.shape[1]} {sky.shape[0]}\n255\n".encode() + sky.tobytes())
+        r = subprocess.run([exe, "bench", "--config", cfg, "--background", bg, "--output", out,
+                            "--worker-counts", "1", "--repeats", str(repeats), "--warmup", "1"],
+                           capture_output=True, text=True, timeout=900,
+                           env=dict(os.environ, BHRT_DEVICES=str(device)))
+        if r.returncode != 0:
+            return {"error": r.stderr.strip()[-300:]}
+        rows = [ln.split(",") for ln in open(out).read().splitlines()[1:]]
+    mean = [float(x[8]) for x in rows if x[7] == "-1"][0]
+    rays = proj.s.width * proj.s.height * proj.s.spp
+    return {"value": rays / mean / 1e6, "unit": "Mrays/s", "seconds_per_run": mean,
+            "runs": [float(x[8]) for x in rows if x[7] != "-1"],
+            "harness": "reference bench.cpp run_strong_scaling(scene, {1}, %d) + emit_csv, "
+                       "RenderRunner = render_image (render_shim.cpp -> C ABI, mode R)" % repeats,
+            "scene": f"sky-only projection of the workload, {proj.s.width}x{proj.s.height}x"
+                     f"{proj.s.spp}, DOPRI5 eps={proj.s.epsilon} windows, 2048x1024 PPM sky, "
+                     f"host image out (wall clock per frame)"}
+
+
 def self_launch(args) -> int:
     """--gpus N outside torchrun: re-launch under torch.distributed.run with N
     ranks, or refuse (non-zero, nothing timed) when fewer GPUs are visible."""
@@ -607,6 +647,9 @@ def run_ours(args):
                          f"[{band[0]},{band[1]}) = {rays} rays, {dt:.1f} s"}
         if not args.no_ref_sky:
             ref_sky = reference_sky_only(scene, threads)
+    harness = None
+    if world == 1 and not args.no_ref_sky:
+        harness = gpu_reference_harness(scene, local)
 
     if world > 1:
         par = (f"cyclic rows x{world}: each rank's kernel stores its rows into rank 0's image "
@@ -634,6 +677,7 @@ def run_ours(args):
                      "flops_per_launch": sum(flops) / len(flops)},
         "cpu_baseline": cpu,
         "reference_sky_only": ref_sky,
+        "reference_harness_gpu": harness,
         "e2e": {"value": e2e_value, "unit": "Mrays/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
                 "api": "FrameRenderer.render (python; pinned host image)"},
@@ -666,7 +710,8 @@ def main():
     ap.add_argument("--ref-rows", type=int, default=None)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-ref-sky", action="store_true",
-                    help="skip the compiled reference's sky-only lattice timing (~10 s)")
+                    help="skip the reference-harness timings: the compiled reference's sky-only "
+                         "lattice (CPU, ~10 s) and the GPU through bhrt_bench_b200 (~10 s)")
     ap.add_argument("--no-secondary", action="store_true")
     args = ap.parse_args()
     if args.gpus < 1:

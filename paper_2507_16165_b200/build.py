@@ -82,15 +82,18 @@ def build_dropin(force: bool = False) -> bool:
       dropin/bhrt_worker_b200         `bhrt worker` (BHRT protocol) on the GPU
       dropin/acceptance_b200          the reference's acceptance suite, its
                                       render.cpp replaced by render_shim.cpp
+      dropin/bhrt_bench_b200          `bhrt bench`: the reference's sweep /
+                                      CSV harness (bench.cpp) timing the GPU
     """
     if not os.path.isdir(os.path.join(REF, "src")):
         return False
     os.makedirs(DROPIN, exist_ok=True)
     shim = os.path.join(CSRC, "render_shim.cpp")
     worker = os.path.join(CSRC, "worker_main.cpp")
+    benchm = os.path.join(CSRC, "bench_main.cpp")
     outs = [os.path.join(DROPIN, n) for n in
-            ("libbhrt_render_b200.so", "bhrt_worker_b200", "acceptance_b200")]
-    deps = [shim, worker, LIB, os.path.join(ROOT, "include", "bhrt_cuda.h")]
+            ("libbhrt_render_b200.so", "bhrt_worker_b200", "acceptance_b200", "bhrt_bench_b200")]
+    deps = [shim, worker, benchm, LIB, os.path.join(ROOT, "include", "bhrt_cuda.h")]
     if not force and all(not _stale(o, deps) for o in outs):
         return True
     cxx = ["g++", "-std=c++20", "-O2", "-fPIC", "-Wno-free-nonheap-object", "-include", "algorithm", "-I" + os.path.join(REF, "include"),
@@ -104,6 +107,7 @@ def build_dropin(force: bool = False) -> bool:
     subprocess.run([*cxx, f'-DBHRT_BINARY="{os.path.join("/root/repo", os.path.relpath(outs[1], ROOT))}"',
                     "-o", outs[2], os.path.join(REF, "tests", "acceptance.cpp"), shim, *srcs, *link],
                    check=True)
+    subprocess.run([*cxx, "-o", outs[3], benchm, shim, *srcs, *link], check=True)
     return True
 
 

@@ -52,6 +52,17 @@ __device__ __forceinline__ double clampd(double v, double lo, double hi) {
 __device__ __forceinline__ double dmax(double a, double b) { return a < b ? b : a; }
 __device__ __forceinline__ double dmin(double a, double b) { return b < a ? b : a; }
 
+// Order tests of doubles on the integer pipe (the FP64 pipe is the step
+// loop's bound). For t > 0 and any x but NaN, x < t, x > t, x >= t agree
+// with the signed comparison of the bit patterns (negative x and -0 pattern
+// below every positive one, positive doubles in increasing order, +inf on
+// top); a +NaN x compares above t (callers say why that cannot change
+// a result).
+__device__ __forceinline__ long long dbits(double x) { return __double_as_longlong(x); }
+__device__ __forceinline__ bool lt_pos(double x, double t) { return dbits(x) < dbits(t); }
+__device__ __forceinline__ bool gt_pos(double x, double t) { return dbits(x) > dbits(t); }
+__device__ __forceinline__ bool ge_pos(double x, double t) { return dbits(x) >= dbits(t); }
+
 // ----------------------------------------------------------------- camera (camera.cpp:10-68)
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
     x += 0x9e3779b97f4a7c15ULL;
@@ -568,7 +579,12 @@ __device__ __forceinline__ bool rkf45_step(double u, double w, double h, double 
     const double du = fma(rtol, dmax(fabs(u), fabs(u_new)), atol);
     const double dw = fma(rtol, dmax(fabs(w), fabs(w_new)), atol);
     const bool err_ok = (fabs(eus) <= du) && (fabs(ews) <= dw);
-    const bool geo_ok = u_new >= 0.5 * u;
+    // u_new >= 0.5 u: for u >= 2^-1021 halving decrements the exponent, and
+    // a NaN u_new has a non-finite error term (the solution and error sums
+    // share their stages, all with nonzero weights), so err_ok is false
+    // whatever geo_ok says
+    const long long bu = dbits(u);
+    const bool geo_ok = bu >= (2LL << 52) ? dbits(u_new) >= bu - (1LL << 52) : u_new >= 0.5 * u;
     const int du_ = (__double2hiint(eus) & 0x7fffffff) - __double2hiint(du);
     const int dw_ = (__double2hiint(ews) & 0x7fffffff) - __double2hiint(dw);
     int q = (du_ > dw_ ? du_ : dw_) >> 18;
@@ -577,7 +593,8 @@ __device__ __forceinline__ bool rkf45_step(double u, double w, double h, double 
     if (err_ok && geo_ok) {
         un = u_new;
         wn = w_new;
-        hn = dmin(h * grow[q - kQMin], hmax);
+        const double hg = h * grow[q - kQMin];  // positive: min by the integer order
+        hn = lt_pos(hmax, hg) ? hmax : hg;
         return true;
     }
     hn = err_ok ? 0.5 * h : h * shrink[q - kQMin];

@@ -591,7 +591,11 @@ __global__ void __launch_bounds__(kBlock, BHRT_SCENE_MINB) trace_scene_kernel(co
                                        wn, hn)) {
                             const double pn = phi + h;
                             ++nsteps;
-                            if (pn < nev_eff && un > p.u_esc && un < p.u_cap && hn >= 1e-14) {
+                            // integer order tests (lt_pos): pn, hn > 0 and u_esc, u_cap >= 0
+                            // (nev_eff may be negative: pn above it either way); a NaN un
+                            // fails un < u_cap and takes the exact tests below
+                            if (lt_pos(pn, nev_eff) & gt_pos(un, p.u_esc) & lt_pos(un, p.u_cap) &
+                                ge_pos(hn, 1e-14)) {
                                 phi = pn;
                                 u = un;
                                 w = wn;
