@@ -588,11 +588,11 @@ def run_ours(args):
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = total_rays / (float(te.item()) * 1e-3) / 1e6
-    staged, params = fr.ctx.upload_bytes()
+    staged, params, counters = fr.ctx.upload_bytes()
     e2e_launches = fr.ctx.stats()["launches"]
-    # scene uploads + kernel parameter blocks + the counters' reset (8 x u64)
-    h2d = staged + e2e_launches * params + 64
-    d2h = (W * H * 3 if rank == 0 else 0) + 64  # the image + the counters
+    # scene uploads + kernel parameter blocks + the counter slots' reset
+    h2d = staged + e2e_launches * params + counters
+    d2h = (W * H * 3 if rank == 0 else 0) + counters  # the image + the counter slots
     peer = fr.peer is not None
 
     # ---- the reference-facing drop-in (C ABI, host buffers), N = 1

@@ -279,9 +279,12 @@ int bhrt_ctx_stats(bhrt_ctx* ctx, uint64_t* steps, uint64_t* rejected, uint64_t*
 int bhrt_ctx_counters(bhrt_ctx* ctx, uint64_t out[8]);
 
 /* Host->device bytes of the last bhrt_ctx_set_scene (pinned-staged uploads:
- * checker cell table, sky texels, spheres, sphere cull table) and the size of
- * the kernel parameter block each launch carries. For e2e byte accounting. */
-int bhrt_ctx_upload_bytes(bhrt_ctx* ctx, uint64_t* staged, uint64_t* params_per_launch);
+ * checker cell table, sky texels, spheres, sphere cull table), the size of
+ * the kernel parameter block each launch carries, and the size of the render
+ * counter block (reset host->device before, read device->host after each
+ * render or frame). For e2e byte accounting. Any pointer may be NULL. */
+int bhrt_ctx_upload_bytes(bhrt_ctx* ctx, uint64_t* staged, uint64_t* params_per_launch,
+                          uint64_t* counter_bytes);
 /* Per-kernel CUDA-event timing of subsequent renders (off by default).
  * After bhrt_ctx_finish, bhrt_ctx_kernel_ms returns the durations of the
  * last render's trace and shade kernels on the render stream. */

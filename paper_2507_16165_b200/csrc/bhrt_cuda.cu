@@ -32,6 +32,7 @@ void launch_cull_build(const KParams& p, CullList* out, cudaStream_t st);
 namespace {
 
 constexpr double kPi = 3.141592653589793;
+constexpr size_t kStatBytes = kStatWords * sizeof(unsigned long long);  // all counter slots
 
 struct HV3 {
     double x, y, z;
@@ -199,7 +200,10 @@ struct bhrt_ctx {
     int pending = 0;
     int32_t last_rows = 0;
     // pinned: [0..7] last render's counters (async D2H), [8..15] their reset pattern
-    unsigned long long* host_stats = nullptr;
+    // pinned: [0, kStatWords) the last render's counter slots (async D2H),
+    // [kStatWords, 2 kStatWords) their reset pattern; folded into stats_sum
+    unsigned long long* host_slots = nullptr;
+    unsigned long long stats_sum[8] = {0, 0, 0, ULLONG_MAX, 0, 0, 0, 0};
     bool in_frame = false;  // bhrt_ctx_frame_begin .. bhrt_ctx_finish: counters accumulate
     int32_t out_image = 0;  // bhrt_ctx_set_output_layout
     // scene uploads: pinned staging -> device on a private non-blocking stream;
@@ -363,15 +367,15 @@ int bhrt_ctx_create(int32_t device, bhrt_ctx** out, bhrt_status_info* info) {
     CK(cudaSetDevice(device));
     std::unique_ptr<bhrt_ctx> c(new bhrt_ctx());
     c->device = device;
-    if (c->stats.ensure(8) || c->tables.ensure(2 * kQN))
+    if (c->stats.ensure(kStatWords) || c->tables.ensure(2 * kQN))
         return set_info(info, BHRT_DEVICE, -1, -1, "bhrt_ctx_create: cudaMalloc failed");
-    CK(cudaMallocHost(&c->host_stats, 16 * sizeof(unsigned long long)));
+    CK(cudaMallocHost(&c->host_slots, 2 * kStatWords * sizeof(unsigned long long)));
     CK(cudaStreamCreateWithFlags(&c->up_stream, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&c->up_done, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->render_done, cudaEventDisableTiming));
     CK(cudaEventRecord(c->up_done, c->up_stream));
-    for (int i = 0; i < 16; ++i) c->host_stats[i] = 0;
-    c->host_stats[3] = c->host_stats[11] = ULLONG_MAX;
+    for (int i = 0; i < 2 * kStatWords; ++i) c->host_slots[i] = 0;
+    c->host_slots[3] = c->host_slots[kStatWords + 3] = ULLONG_MAX;
     double tb[2 * kQN];
     factor_tables(tb, tb + kQN);
     CK(cudaMemcpy(c->tables.p, tb, sizeof tb, cudaMemcpyHostToDevice));
@@ -425,7 +429,7 @@ void bhrt_ctx_destroy(bhrt_ctx* c) {
     c->defl.release();
     c->poly_pts.release();
     c->poly_n.release();
-    if (c->host_stats) cudaFreeHost(c->host_stats);
+    if (c->host_slots) cudaFreeHost(c->host_slots);
     if (c->staging) cudaFreeHost(c->staging);
     if (c->up_done) cudaEventDestroy(c->up_done);
     if (c->render_done) cudaEventDestroy(c->render_done);
@@ -662,7 +666,7 @@ int bhrt_ctx_render_async(bhrt_ctx* c, int32_t row_start, int32_t row_end, int32
     k.stats = c->stats.p;
     CK(cudaStreamWaitEvent(st, c->up_done, 0));  // the scene's uploads
     if (!c->in_frame) {  // counters + lowest failing pixel start fresh for this render
-        CK(cudaMemcpyAsync(c->stats.p, c->host_stats + 8, 8 * sizeof(unsigned long long),
+        CK(cudaMemcpyAsync(c->stats.p, c->host_slots + kStatWords, kStatBytes,
                            cudaMemcpyHostToDevice, st));
         c->launches = 0;
     }
@@ -681,7 +685,7 @@ int bhrt_ctx_render_async(bhrt_ctx* c, int32_t row_start, int32_t row_end, int32
         }
         CK(cudaEventRecord(c->frame_ev[c->frame_nev++], st));
     } else {
-        CK(cudaMemcpyAsync(c->host_stats, c->stats.p, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+        CK(cudaMemcpyAsync(c->host_slots, c->stats.p, kStatBytes, cudaMemcpyDeviceToHost,
                            st));
         CK(cudaEventRecord(c->render_done, st));
     }
@@ -749,12 +753,21 @@ int bhrt_ctx_frame_begin(bhrt_ctx* c, void* stream, bhrt_status_info* info) {
     if (!c || !c->has_scene) return set_info(info, BHRT_INVALID_ARGUMENT, -1, -1, "context has no scene");
     CK(cudaSetDevice(c->device));
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    CK(cudaMemcpyAsync(c->stats.p, c->host_stats + 8, 8 * sizeof(unsigned long long), cudaMemcpyHostToDevice,
+    CK(cudaMemcpyAsync(c->stats.p, c->host_slots + kStatWords, kStatBytes, cudaMemcpyHostToDevice,
                        st));
     c->launches = 0;
     c->in_frame = true;
     c->frame_nev = 0;
     return 0;
+}
+
+// Counter slots (kStatSlots, kernel side warp_add_stats) -> the 8 counters:
+// sums, except the lowest failing pixel (slot 0 only, atomicMin).
+static void fold_stats(bhrt_ctx* c) {
+    for (int w = 0; w < 8; ++w) c->stats_sum[w] = c->host_slots[w];
+    for (int s = 1; s < kStatSlots; ++s)
+        for (int w = 0; w < 8; ++w)
+            if (w != 3) c->stats_sum[w] += c->host_slots[kStatStride * s + w];
 }
 
 // The reference's failure text for the lowest failing pixel (render.cpp:36-40
@@ -789,7 +802,7 @@ static void failure_text(bhrt_ctx* c, int px, int py, char* out, size_t cap) {
     k.diag = 1;            // the diagnostic kernel instantiations
     std::vector<bhrt_ray_record> h(k.spp);
     int launches = 0;
-    bool ok = cudaMemcpyAsync(c->stats.p, c->host_stats + 8, 8 * sizeof(unsigned long long),
+    bool ok = cudaMemcpyAsync(c->stats.p, c->host_slots + kStatWords, kStatBytes,
                               cudaMemcpyHostToDevice, c->up_stream) == cudaSuccess &&
               launch_trace(k, c->up_stream, &launches, nullptr) == 0 &&
               cudaMemcpyAsync(h.data(), rec.p + static_cast<size_t>(px) * k.spp,
@@ -818,7 +831,7 @@ int bhrt_ctx_finish(bhrt_ctx* c, bhrt_status_info* info) {
     CK(cudaSetDevice(c->device));
     if (c->in_frame && c->pending) {
         for (size_t i = 0; i < c->frame_nev; ++i) CK(cudaEventSynchronize(c->frame_ev[i]));
-        CK(cudaMemcpyAsync(c->host_stats, c->stats.p, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+        CK(cudaMemcpyAsync(c->host_slots, c->stats.p, kStatBytes, cudaMemcpyDeviceToHost,
                            c->up_stream));
         CK(cudaStreamSynchronize(c->up_stream));
         CK(cudaEventRecord(c->render_done, c->up_stream));
@@ -828,7 +841,8 @@ int bhrt_ctx_finish(bhrt_ctx* c, bhrt_status_info* info) {
     if (!c->pending) return 0;
     CK(cudaEventSynchronize(c->render_done));  // this render only, not later work on the stream
     c->pending = 0;
-    const unsigned long long fail = c->host_stats[3];  // lowest failing y * width + x
+    fold_stats(c);
+    const unsigned long long fail = c->stats_sum[3];  // lowest failing y * width + x
     if (fail != ULLONG_MAX) {
         const int py = static_cast<int>(fail / c->kp.width);
         const int px = static_cast<int>(fail % c->kp.width);
@@ -840,24 +854,25 @@ int bhrt_ctx_finish(bhrt_ctx* c, bhrt_status_info* info) {
     return 0;
 }
 
-int bhrt_ctx_upload_bytes(bhrt_ctx* c, uint64_t* staged, uint64_t* params_per_launch) {
+int bhrt_ctx_upload_bytes(bhrt_ctx* c, uint64_t* staged, uint64_t* params_per_launch, uint64_t* counter_bytes) {
     if (!c) return BHRT_INVALID_ARGUMENT;
     if (staged) *staged = c->upload_bytes;
     if (params_per_launch) *params_per_launch = sizeof(KParams);
+    if (counter_bytes) *counter_bytes = kStatBytes;
     return 0;
 }
 
 int bhrt_ctx_counters(bhrt_ctx* c, uint64_t out[8]) {
     if (!c) return BHRT_INVALID_ARGUMENT;
-    for (int i = 0; i < 8; ++i) out[i] = c->host_stats[i];
+    for (int i = 0; i < 8; ++i) out[i] = c->stats_sum[i];
     return 0;
 }
 
 int bhrt_ctx_stats(bhrt_ctx* c, uint64_t* steps, uint64_t* rejected, uint64_t* rays, int32_t* launches) {
     if (!c) return BHRT_INVALID_ARGUMENT;
-    if (steps) *steps = c->host_stats[0];
-    if (rejected) *rejected = c->host_stats[1];
-    if (rays) *rays = c->host_stats[2];
+    if (steps) *steps = c->stats_sum[0];
+    if (rejected) *rejected = c->stats_sum[1];
+    if (rays) *rays = c->stats_sum[2];
     if (launches) *launches = c->launches;
     return 0;
 }

@@ -277,9 +277,10 @@ __device__ __forceinline__ void warp_add_stats(unsigned long long* stats, unsign
         }
     }
     if ((threadIdx.x & 31) == 0) {
-        atomicAdd(&stats[0], s);
-        atomicAdd(&stats[1], r);
-        atomicAdd(&stats[2], n);
+        unsigned long long* slot = stats + kStatStride * (blockIdx.x & (kStatSlots - 1));
+        atomicAdd(&slot[0], s);
+        atomicAdd(&slot[1], r);
+        atomicAdd(&slot[2], n);
     }
 }
 
@@ -378,24 +379,42 @@ __device__ static BHRT_INL_SHADE void shade_sample(const KParams& p, int obj, in
                 // cell indices without atan2/asin: cu = #{k : atan2(z,x) >= theta_k},
                 // cv = #{k : y <= cos(pi k / nv)}, thresholds from the host;
                 // equal to the floor() form except within ulps of a cell edge
+                // Both counts are monotone in k (ge(0) and y <= tab_v[0] = 1
+                // always hold), so an fp32 estimate k0 whose exact tests give
+                // ge(k0) && !ge(k0 + 1) is the count; the binary search decides
+                // the rest (directions within ~1e-5 rad of a cell edge).
                 const bool upper = !signbit(pt.z);  // atan2's half plane
-                int lo = 0, hi = p.checker_nu;      // count in [lo, hi)
-                while (hi - lo > 1) {
-                    const int k = (lo + hi) >> 1;
+                auto ge_u = [&](int k) {
                     const double ck = __ldg(p.checker_tab + k), sk = __ldg(p.checker_tab + kCheckerMax + k);
                     const bool kup = sk > 0.0 || (sk == 0.0 && ck > 0.0);
-                    const bool ge = upper != kup ? upper : (ck * pt.z - sk * pt.x >= 0.0);
-                    if (ge) lo = k; else hi = k;
-                }
-                cu = lo;
-                lo = 0;
-                hi = p.checker_nv;
+                    return upper != kup ? upper : (ck * pt.z - sk * pt.x >= 0.0);
+                };
+                const int nu = p.checker_nu, nv = p.checker_nv;
                 const double y = clampd(pt.y, -1.0, 1.0);
-                while (hi - lo > 1) {
-                    const int k = (lo + hi) >> 1;
-                    if (y <= __ldg(p.checker_tab + 2 * kCheckerMax + k)) lo = k; else hi = k;
+                auto le_v = [&](int k) { return y <= __ldg(p.checker_tab + 2 * kCheckerMax + k); };
+                const float fu = (atan2f((float)pt.z, (float)pt.x) + 3.14159265f) * (0.15915494f * (float)nu);
+                const float fv = acosf((float)y) * (0.31830989f * (float)nv);
+                const int ku = min(max((int)fu, 0), nu - 1), kv = min(max((int)fv, 0), nv - 1);
+                if ((ku == 0 || ge_u(ku)) && (ku + 1 >= nu || !ge_u(ku + 1))) {
+                    cu = ku;
+                } else {
+                    int lo = 0, hi = nu;  // count in [lo, hi)
+                    while (hi - lo > 1) {
+                        const int k = (lo + hi) >> 1;
+                        if (ge_u(k)) lo = k; else hi = k;
+                    }
+                    cu = lo;
                 }
-                cv = lo;
+                if ((kv == 0 || le_v(kv)) && (kv + 1 >= nv || !le_v(kv + 1))) {
+                    cv = kv;
+                } else {
+                    int lo = 0, hi = nv;
+                    while (hi - lo > 1) {
+                        const int k = (lo + hi) >> 1;
+                        if (le_v(k)) lo = k; else hi = k;
+                    }
+                    cv = lo;
+                }
             } else {
                 const double u_tex = (atan2(pt.z, pt.x) + PI_D) / (2.0 * PI_D);
                 const double v_tex = (PI_D / 2.0 - asin(clampd(pt.y, -1.0, 1.0))) / PI_D;

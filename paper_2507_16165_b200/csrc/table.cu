@@ -291,7 +291,14 @@ __global__ void __launch_bounds__(128, BHRT_TAB_MINB) trace_table_kernel(const _
             const double u0 = p.cam_u0, w0 = F.w;
             const double M2 = 2.0 * p.mass;
             const double energy = w0 * w0 + u0 * u0 - M2 * u0 * u0 * u0;
+#ifdef BHRT_EXPERIMENT_NOTAB
+            if (energy != -12345.0) {  // timing experiment only: setup + shading, no table
+                obj = BHRT_OBJ_SKY;
+                point = unit_fast(D);
+            } else if (!(energy > 0.0)) {
+#else
             if (!(energy > 0.0)) {
+#endif
                 obj = BHRT_OBJ_STALLED;
             } else {
                 const double b = 1.0 / sqrt(energy);

@@ -71,7 +71,7 @@ def lib():
         L.bhrt_ctx_stats.argtypes = [C.c_void_p, P(C.c_uint64), P(C.c_uint64), P(C.c_uint64),
                                      P(C.c_int32)]
         L.bhrt_ctx_counters.argtypes = [C.c_void_p, P(C.c_uint64)]
-        L.bhrt_ctx_upload_bytes.argtypes = [C.c_void_p, P(C.c_uint64), P(C.c_uint64)]
+        L.bhrt_ctx_upload_bytes.argtypes = [C.c_void_p, P(C.c_uint64), P(C.c_uint64), P(C.c_uint64)]
         L.bhrt_ctx_set_timing.argtypes = [C.c_void_p, C.c_int32]
         L.bhrt_ctx_kernel_ms.argtypes = [C.c_void_p, P(C.c_float), P(C.c_float)]
         L.bhrt_tile_row_count.argtypes = [C.c_int32] * 5

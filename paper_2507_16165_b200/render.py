@@ -187,12 +187,12 @@ class Context:
             raise native.BhrtError(rc, -1, -1, "kernel timing unavailable")
         return a.value, b.value
 
-    def upload_bytes(self) -> tuple[int, int]:
+    def upload_bytes(self) -> tuple[int, int, int]:
         """(bytes staged host->device by the last set_scene, kernel parameter
-        bytes per launch) — bhrt_ctx_upload_bytes."""
-        a, b = C.c_uint64(), C.c_uint64()
-        native.lib().bhrt_ctx_upload_bytes(self._h, C.byref(a), C.byref(b))
-        return a.value, b.value
+        bytes per launch, render counter block bytes) — bhrt_ctx_upload_bytes."""
+        a, b, c = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        native.lib().bhrt_ctx_upload_bytes(self._h, C.byref(a), C.byref(b), C.byref(c))
+        return a.value, b.value, c.value
 
     def counters(self) -> list[int]:
         out = (C.c_uint64 * 8)()

@@ -11,20 +11,23 @@ FL="-O3 -std=c++17 -lineinfo --fmad=false -Xcompiler -fPIC,-ffp-contract=off -Ii
 for spec in "$@"; do
   name=${spec%%:*}; defs=${spec#*:}; defs=${defs//,/ }
   src=paper_2507_16165_b200/csrc
+  inc=include
   if [[ "$name" == *@* ]]; then
     ref=${name#*@}; name=${name%%@*}
-    src=build/variants/src_$name
-    rm -rf "$src"; mkdir -p "$src"
-    git archive "$ref" paper_2507_16165_b200/csrc | tar -x -C "$src" --strip-components=2
+    root=build/variants/src_$name
+    rm -rf "$root"; mkdir -p "$root"
+    git archive "$ref" paper_2507_16165_b200/csrc include | tar -x -C "$root"
+    src=$root/paper_2507_16165_b200/csrc
+    inc=$root/include
   fi
   objs=""
   for f in trace_reference.cu trace_scene.cu table.cu shade.cu bhrt_cuda.cu fp64_peak.cu scene_text.cpp; do
-    nvcc $ARCH $FL -I$src $defs -c $src/$f -o build/variants/${name}_${f%.*}.o &
+    nvcc $ARCH ${FL/-Iinclude/-I$inc} -I$src $defs -c $src/$f -o build/variants/${name}_${f%.*}.o &
     objs="$objs build/variants/${name}_${f%.*}.o"
   done
   wait
   nvcc $ARCH -shared -o build/variants/lib_$name.so $objs -lcudart
   rm -f $objs
-  [[ "$src" == build/variants/src_* ]] && rm -rf "$src"
+  [[ "$src" == build/variants/src_* ]] && rm -rf "build/variants/src_$name"
   echo built build/variants/lib_$name.so
 done

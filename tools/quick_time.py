@@ -28,7 +28,7 @@ def main():
         e1.synchronize()  # finish() waits for the render only; the end event may trail it
         ms = e0.elapsed_time(e1)
         s = ctx.stats()
-        rays = s["rays"]
+        rays = sb.s.width * sb.s.height * sb.s.spp  # (counters may be compiled out in experiments)
         print(f"config {idx} rep {r}: {ms:.2f} ms  {rays / ms / 1e3:.1f} Mrays/s  "
               f"steps/ray {s['steps'] / rays:.2f} rej/ray {s['rejected'] / rays:.3f}", flush=True)
 
