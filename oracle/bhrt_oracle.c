@@ -762,9 +762,11 @@ static void ray_events_setup(scene_ray_t* R) {
             const double pl = atan2_est(ly, lx);
             R->next_disk = pl > 0.0 ? pl : pl + PI;
             R->disk_sigma = pl > 0.0 ? 1.0 : -1.0;
-            R->disk_lx = lx / nl;
-            R->disk_ly = ly / nl;
-            R->disk_L = dvd(add(scl(R->e1, lx), scl(R->e2, ly)), nl);
+            /* one reciprocal for the unit line (plane and world coordinates) */
+            const double inl = 1.0 / nl;
+            R->disk_lx = lx * inl;
+            R->disk_ly = ly * inl;
+            R->disk_L = scl(add(scl(R->e1, lx), scl(R->e2, ly)), inl);
         }
     }
     R->nc = 0;

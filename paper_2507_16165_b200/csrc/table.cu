@@ -95,12 +95,25 @@ __device__ double inbound_psi(const TabView& T, int e, double target) {
     return (double)j * T.dpsi + h * t;
 }
 
+// One entry's per-frame metadata, loaded together as soon as the entry index
+// is known (independent loads: one memory latency instead of a chain).
+struct TabEntry {
+    int kind, n;
+    double pend, pesc, psi0;  // ends[0], ends[3], the camera's inbound psi
+};
+
+__device__ __forceinline__ TabEntry tab_entry(const TabView& T, const double* psi0, int e) {
+    const double2 e01 = __ldg(reinterpret_cast<const double2*>(T.ends + 4 * (size_t)e));
+    const double2 e23 = __ldg(reinterpret_cast<const double2*>(T.ends + 4 * (size_t)e + 2));
+    return {__ldg(&T.kind[e]), __ldg(&T.n[e]), e01.x, e23.y, __ldg(&psi0[e])};
+}
+
 // oracle table_u: u on entry e at orbit angle psi (mirrored past periapsis).
-__device__ double table_u(const TabView& T, int e, double psi) {
-    const int kind = __ldg(&T.kind[e]), n = __ldg(&T.n[e]);
+__device__ double table_u(const TabView& T, int e, const TabEntry& M, double psi) {
+    const int kind = M.kind, n = M.n;
     const double* S = T.smp + (size_t)e * T.ns * 2;
     const double* E = T.ends + 4 * (size_t)e;
-    const double pend = __ldg(&E[0]);
+    const double pend = M.pend;
     if (kind == 1 && psi > pend) psi = 2.0 * pend - psi;
     if (psi < 0.0 || n < 1) return -1.0;
     int j = (int)floor(div_by(psi, T.dpsi, T.inv_dpsi));
@@ -222,16 +235,15 @@ __global__ void bind_table_kernel(const __grid_constant__ KParams p, double* end
 }
 
 // oracle table_plan
-__device__ __forceinline__ bool table_plan(const TabView& T, int e, double psi0, double w0, int& outcome,
-                                           double& phi_end) {
-    const int kind = __ldg(&T.kind[e]);
-    const double* E = T.ends + 4 * (size_t)e;
+__device__ __forceinline__ bool table_plan(const TabEntry& M, double w0, int& outcome, double& phi_end) {
+    const int kind = M.kind;
+    const double psi0 = M.psi0;
     if (kind == 3 || psi0 < 0.0) return false;
-    const double pesc = __ldg(&E[3]);
+    const double pesc = M.pesc;
     if (w0 >= 0.0) {
         if (kind == 0) {
             outcome = BHRT_OBJ_HORIZON;
-            phi_end = __ldg(&E[0]) - psi0;
+            phi_end = M.pend - psi0;
             return true;
         }
         if (kind == 2) {
@@ -241,7 +253,7 @@ __device__ __forceinline__ bool table_plan(const TabView& T, int e, double psi0,
         }
         if (pesc < 0.0) return false;
         outcome = BHRT_OBJ_SKY;
-        phi_end = (2.0 * __ldg(&E[0]) - pesc) - psi0;
+        phi_end = (2.0 * M.pend - pesc) - psi0;
         return true;
     }
     if (pesc < 0.0) return false;
@@ -251,7 +263,7 @@ __device__ __forceinline__ bool table_plan(const TabView& T, int e, double psi0,
 }
 
 #ifndef BHRT_TAB_MINB
-#define BHRT_TAB_MINB 6  // 1/6/8/10 blocks -> 2.36/2.34/2.41/2.54 ms (config 3)
+#define BHRT_TAB_MINB 7  // 5/6/7/8/10/12 blocks -> 1.76/1.67/1.56/1.56/1.73/1.94 ms (config 3)
 #endif
 __global__ void __launch_bounds__(128, BHRT_TAB_MINB) trace_table_kernel(const __grid_constant__ KParams p) {
     const long long n = (long long)p.n_rows * p.width * p.spp;
@@ -304,16 +316,14 @@ __global__ void __launch_bounds__(128, BHRT_TAB_MINB) trace_table_kernel(const _
                 const double b = 1.0 / sqrt(energy);
                 // disk line (oracle ray_events_setup)
                 double next_disk = CUDART_INF, sigma = 1.0;
-                V3 Lw = mk(0.0, 0.0, 0.0);
+                const double lx = -e2.y, ly = e1.y;  // (L.e1, L.e2), oracle ray_events_setup
                 if (p.disk_enabled) {
-                    const double lx = -e2.y, ly = e1.y;  // (L.e1, L.e2), oracle ray_events_setup
                     const double nl2 = lx * lx + ly * ly;
                     if (nl2 >= 1e-24) {  // |L| >= 1e-12
-                        const double nl = sqrt(nl2);
                         const double pl = atan2_est(ly, lx);
                         next_disk = pl > 0.0 ? pl : pl + PI_D;
                         sigma = pl > 0.0 ? 1.0 : -1.0;
-                        Lw = dvd(add(scl(e1, lx), scl(e2, ly)), nl);
+                        // the unit line L/|L| is formed only on a disk hit (below)
                     }
                 }
                 const int N = p.table_entries;
@@ -321,13 +331,14 @@ __global__ void __launch_bounds__(128, BHRT_TAB_MINB) trace_table_kernel(const _
                 int ie = (int)floor(x);
                 if (ie > N - 2) ie = N - 2;
                 BHRT_ASSERT(ie >= 0 && ie + 1 < N);
+                const TabEntry Mi = tab_entry(T, p.tab_psi0, ie), Mj = tab_entry(T, p.tab_psi0, ie + 1);
                 double f = x - (double)ie;
-                if (__ldg(&p.tab_kind[ie]) == 3) f = 1.0;
-                const double p0i = __ldg(&p.tab_psi0[ie]), p0j = __ldg(&p.tab_psi0[ie + 1]);
+                if (Mi.kind == 3) f = 1.0;
+                const double p0i = Mi.psi0, p0j = Mj.psi0;
                 int oi = 0, oj = 0;
                 double pi_ = 0.0, pj = 0.0;
-                const bool vi = table_plan(T, ie, p0i, w0, oi, pi_);
-                const bool vj = table_plan(T, ie + 1, p0j, w0, oj, pj);
+                const bool vi = table_plan(Mi, w0, oi, pi_);
+                const bool vj = table_plan(Mj, w0, oj, pj);
                 int outcome = BHRT_OBJ_STALLED;
                 double phi_end = 0.0, wi = 0.0, wj = 0.0;
                 bool ok = true;
@@ -364,8 +375,8 @@ __global__ void __launch_bounds__(128, BHRT_TAB_MINB) trace_table_kernel(const _
                         if (wi > 0.0) ui = 0.01 * (1.0 + ph);
                         if (wj > 0.0) uj = 0.01 * (1.0 + ph);
 #else
-                        if (wi > 0.0) ui = table_u(T, ie, p0i + sgn * ph);
-                        if (wj > 0.0) uj = table_u(T, ie + 1, p0j + sgn * ph);
+                        if (wi > 0.0) ui = table_u(T, ie, Mi, p0i + sgn * ph);
+                        if (wj > 0.0) uj = table_u(T, ie + 1, Mj, p0j + sgn * ph);
 #endif
                         nevals += (wi > 0.0) + (wj > 0.0);
                         double u_ev;
@@ -377,6 +388,8 @@ __global__ void __launch_bounds__(128, BHRT_TAB_MINB) trace_table_kernel(const _
                             const double r_ev = 1.0 / u_ev;
                             if (r_ev >= p.disk_r_in && r_ev <= p.disk_r_out) {
                                 obj = BHRT_OBJ_DISK;
+                                const double inl = 1.0 / sqrt(lx * lx + ly * ly);  // oracle ray_events_setup
+                                const V3 Lw = scl(add(scl(e1, lx), scl(e2, ly)), inl);
                                 point = add(O, scl(Lw, sigma * r_ev));
                                 phi_out = ph;
                                 hit = true;

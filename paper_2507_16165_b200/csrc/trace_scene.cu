@@ -160,10 +160,10 @@ template <class SM>
 __device__ __forceinline__ void disk_line(const KParams& p, const SM& sm, int t, double& dlx, double& dly, V3& Lw) {
     const V3 e1 = vld(p.cam_e1), e2 = ld3(sm.e2, t);
     const double lx = -e2.y, ly = e1.y;
-    const double nl = sqrt(lx * lx + ly * ly);
-    dlx = lx / nl;
-    dly = ly / nl;
-    Lw = dvd(add(scl(e1, lx), scl(e2, ly)), nl);
+    const double inl = 1.0 / sqrt(lx * lx + ly * ly);  // one reciprocal (oracle ray_events_setup)
+    dlx = lx * inl;
+    dly = ly * inl;
+    Lw = scl(add(scl(e1, lx), scl(e2, ly)), inl);
 }
 
 // Sphere half of step_events(): first entering hit on the step's S
