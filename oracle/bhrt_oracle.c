@@ -1393,7 +1393,8 @@ static void shade_object(const bhrt_scene* s, const prep_t* P, const scene_ray_t
         case BHRT_OBJ_DISK: {
             const v3 q = sub(R->point, R->O);
             const double r = sqrt(q.x * q.x + q.z * q.z);
-            const double t = (r - s->disk_r_in) / (s->disk_r_out - s->disk_r_in);
+            /* the ramp scale is one reciprocal per scene (the kernels take it from the host) */
+            const double t = (r - s->disk_r_in) * (1.0 / (s->disk_r_out - s->disk_r_in));
             for (int c = 0; c < 3; ++c)
                 rgb[c] = s->disk_color_in[c] + t * (s->disk_color_out[c] - s->disk_color_in[c]);
             break;

@@ -525,6 +525,7 @@ int bhrt_ctx_set_scene(bhrt_ctx* c, const bhrt_scene* s, bhrt_status_info* info)
     k.disk_enabled = s->disk_enabled;
     k.disk_r_in = s->disk_r_in;
     k.disk_r_out = s->disk_r_out;
+    k.disk_inv_width = 1.0 / (s->disk_r_out - s->disk_r_in);
     std::memcpy(k.disk_c_in, s->disk_color_in, sizeof k.disk_c_in);
     std::memcpy(k.disk_c_out, s->disk_color_out, sizeof k.disk_c_out);
     k.n_spheres = s->n_spheres;

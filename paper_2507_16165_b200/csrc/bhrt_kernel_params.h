@@ -83,6 +83,7 @@ struct KParams {
     int32_t disk_enabled;
     int32_t n_spheres;
     double disk_r_in, disk_r_out;
+    double disk_inv_width;  // 1 / (disk_r_out - disk_r_in), the colour ramp's scale (oracle shade)
     double disk_c_in[3], disk_c_out[3];
     // spheres (device arrays)
     const bhrt_sphere* spheres;

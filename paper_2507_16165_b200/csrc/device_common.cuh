@@ -433,7 +433,7 @@ __device__ static BHRT_INL_SHADE void shade_sample(const KParams& p, int obj, in
     } else if (obj == BHRT_OBJ_DISK) {
         const V3 q = sub(pt, vld(p.center));
         const double rr = sqrt(q.x * q.x + q.z * q.z);
-        const double t = (rr - p.disk_r_in) / (p.disk_r_out - p.disk_r_in);
+        const double t = (rr - p.disk_r_in) * p.disk_inv_width;  // oracle: one host reciprocal
 #pragma unroll
         for (int c = 0; c < 3; ++c) rgb[c] = p.disk_c_in[c] + t * (p.disk_c_out[c] - p.disk_c_in[c]);
     } else if (obj == BHRT_OBJ_SPHERE) {
