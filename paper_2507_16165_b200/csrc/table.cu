@@ -406,7 +406,8 @@ __global__ void __launch_bounds__(128, BHRT_TAB_MINB) trace_table_kernel(const _
                             const double ue = p.u_esc;
                             const double q = energy - ue * ue + M2 * ue * ue * ue;
                             const double ws = -sqrt(q > 0.0 ? q : 0.0);
-                            const double c = cos(phi_end), sn = sin(phi_end);
+                            double c, sn;
+                            sincos(phi_end, &sn, &c);  // one argument reduction (libdevice sin/cos values)
                             const double tx = -ue * sn - ws * c, ty = ue * c - ws * sn;
                             point = unit_fast(add(scl(e1, tx), scl(e2, ty)));
                         }
