@@ -33,6 +33,11 @@ constexpr float kWinMargin = 5e-4f;  // fp32 window slack (rad); windows only cu
 // 3 -> 10.3, 4 -> 8.83, 5 -> 8.65, 6 -> 9.12 ms (5 spills only outside the step)
 #define BHRT_SCENE_MINB 5
 #endif
+#ifndef BHRT_SCENE_MINB_RK4
+// the RK4 instantiation (config 0: few long latency-bound rays) keeps more
+// registers: 2 / 3 / 4 / 5 / 6 blocks per SM -> 1.21 / 1.21 / 1.22 / 1.34 / 1.48 ms
+#define BHRT_SCENE_MINB_RK4 4
+#endif
 
 // Per-ray slots (lane-major: slot index = ray's position in the block, so
 // a warp's 32 accesses hit 32 consecutive words — conflict-free).
@@ -469,7 +474,8 @@ __device__ __noinline__ Hit radial_scene(const KParams& p, V3 origin, V3 dir, do
 // in their point for the host's failure text; the production instantiation
 // keeps nothing extra alive on those exits.
 template <int INTEG, bool DIAG>
-__global__ void __launch_bounds__(kBlock, BHRT_SCENE_MINB) trace_scene_kernel(const __grid_constant__ KParams p) {
+__global__ void __launch_bounds__(kBlock, INTEG == BHRT_INTEGRATOR_RK4 ? BHRT_SCENE_MINB_RK4 : BHRT_SCENE_MINB)
+    trace_scene_kernel(const __grid_constant__ KParams p) {
     __shared__ SceneSm sm;
     const int t = threadIdx.x;
 
