@@ -103,6 +103,9 @@ __device__ BHRT_INL_SETUP double events_setup(const KParams& p, SM& sm, int t, V
             // the unit line (lx/nl, ly/nl) and L/nl are formed at hit time (disk_line)
         }
     }
+#ifdef BHRT_EXPERIMENT_NODISKEV
+    next_disk = CUDART_INF;  // timing experiment only: no disk events
+#endif
     sm.next_disk[t] = next_disk;
     int nc = 0;
     float next_sph = CUDART_INF_F;
@@ -416,6 +419,9 @@ template <class SM>
 __device__ BHRT_INL_ESC V3 escape_dir(const KParams& p, SM& sm, int t, bool has_step, double pa,
                                       double ua, double wa, double pb, double ub, double wb) {
     const V3 e1 = vld(p.cam_e1), e2 = ld3(sm.e2, t);
+#ifdef BHRT_EXPERIMENT_NOESC
+    if (ua != -1.0) return e1;  // timing experiment only: no escape direction
+#endif
     if (!has_step || !(ua > p.u_esc)) return tangent_dir(e1, e2, pb, ub, wb);
     const double u_esc = p.u_esc;
     const double h = pb - pa;
