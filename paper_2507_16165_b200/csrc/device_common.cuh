@@ -598,12 +598,7 @@ __device__ __forceinline__ bool rkf45_step(double u, double w, double h, double 
     const double du = fma(rtol, dmax(fabs(u), fabs(u_new)), atol);
     const double dw = fma(rtol, dmax(fabs(w), fabs(w_new)), atol);
     const bool err_ok = (fabs(eus) <= du) && (fabs(ews) <= dw);
-    // u_new >= 0.5 u: for u >= 2^-1021 halving decrements the exponent, and
-    // a NaN u_new has a non-finite error term (the solution and error sums
-    // share their stages, all with nonzero weights), so err_ok is false
-    // whatever geo_ok says
-    const long long bu = dbits(u);
-    const bool geo_ok = bu >= (2LL << 52) ? dbits(u_new) >= bu - (1LL << 52) : u_new >= 0.5 * u;
+    const bool geo_ok = u_new >= 0.5 * u;  // (the integer form: more instructions, 5.97 vs 5.92 ms)
     const int du_ = (__double2hiint(eus) & 0x7fffffff) - __double2hiint(du);
     const int dw_ = (__double2hiint(ews) & 0x7fffffff) - __double2hiint(dw);
     int q = (du_ > dw_ ? du_ : dw_) >> 18;
