@@ -61,3 +61,29 @@ def test_back_to_back_unfused_renders():
         ctx.finish()
         assert np.array_equal(out.cpu().numpy(), ref)
     ctx.close()
+
+
+@pytest.mark.parametrize("kind", ["rk4", "rkf45", "table", "modeR"])
+def test_counter_slots_fold_to_frame_totals(kind):
+    """The render counters are spread over line-separated slots (one per
+    block mod kStatSlots) and folded on the host: rays = every sample of the
+    frame, steps = the sum of the per-sample step counts of the records path
+    (integration kernels), over a frame of many blocks and across renders."""
+    import torch
+    sb = {"rk4": lambda: scenes.config(0, 160, 90), "rkf45": lambda: scenes.config(2, 320, 180),
+          "table": lambda: scenes.config(3, 320, 180),
+          "modeR": lambda: scenes.sky_only_projection(scenes.config(2, 96, 54))}[kind]()
+    W, H, spp = sb.s.width, sb.s.height, sb.s.spp
+    ctx = render.Context(0)
+    ctx.set_scene(sb)
+    out = torch.zeros(W * H * 3, dtype=torch.uint8, device="cuda")
+    for _ in range(2):  # the second render starts from reset slots
+        ctx.render_async(out.data_ptr())
+        ctx.finish()
+        st = ctx.stats()
+        assert st["rays"] == W * H * spp
+    ctx.close()
+    if kind != "table":  # table mode records carry no step counts
+        _, rec = render.render_rows(sb, 0, H, 1, records=True)
+        assert st["steps"] == int(rec["steps"].astype(np.int64).sum())
+    assert st["steps"] > 0
