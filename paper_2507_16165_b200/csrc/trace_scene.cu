@@ -284,24 +284,11 @@ __device__ BHRT_INL_EVT bool step_events(const KParams& p, SM& sm, int t, double
                                          double wa, double pb, double ub, double wb, double& next_ev,
                                          Hit& hit) {
     const double h = pb - pa;
-    const Cubic cu = hermite_coef(h, ua, wa, ub, wb);
     double next_disk = sm.next_disk[t];
 #ifdef BHRT_COUNTERS
     atomicAdd(&p.stats[7], 1ull);
 #endif
-    // ---- disk (only the radius is kept across the sphere search; the disk
-    // line is formed after it, so little stays live across that call)
-    bool disk_hit = false;
-    double r_ev;
-    const double sigma = sm.sigma[t];
-    if (next_disk > pa && next_disk <= pb) {
-        const double tt = (next_disk - pa) / h;
-        const double u_ev = hermite_eval(cu, tt);
-        if (u_ev > 0.0) {
-            r_ev = 1.0 / u_ev;
-            disk_hit = r_ev >= p.disk_r_in && r_ev <= p.disk_r_out;
-        }
-    }
+    const bool disk_in = next_disk > pa && next_disk <= pb;
     // ---- spheres
     const int nc = sm.nc[t];
     const bool test_all = nc < 0;
@@ -310,11 +297,45 @@ __device__ BHRT_INL_EVT bool step_events(const KParams& p, SM& sm, int t, double
     // so the sphere half is skipped entirely — disk-only event steps.
     const bool sph_here = test_all || sm.next_sph[t] <= (float)pb;
     unsigned act = 0;
-    unsigned ang = 0;  // candidates whose angular window meets the step
+    unsigned ang = 0;   // candidates whose angular window meets the step
+    unsigned pass = 0;  // candidates whose window ends inside the step (moved on below)
+    float next_sph = sm.next_sph[t];
     if (!test_all && sph_here) {
+        // one pass over the slots: the angular test, and the next window
+        // start after this step (a window ending before pb moves on by 2 pi,
+        // stored after the search, which reads the windows as they are)
         const float fa = (float)pa, fb = (float)pb;
-        for (int i = 0; i < nc; ++i)
-            if (sm.lo[i][t] <= fb && sm.hi[i][t] >= fa) ang |= 1u << i;
+        next_sph = CUDART_INF_F;
+        for (int i = 0; i < nc; ++i) {
+            float lo = sm.lo[i][t];
+            float hi = sm.hi[i][t];
+            if (lo <= fb && hi >= fa) ang |= 1u << i;
+            if (hi < fb) {
+                pass |= 1u << i;
+                while (hi < fb) {
+                    lo += 2.0f * (float)PI_D;
+                    hi += 2.0f * (float)PI_D;
+                }
+            }
+            next_sph = fminf(next_sph, lo);
+        }
+    }
+    // the step's Hermite interpolant, needed for a disk crossing, a window
+    // meeting the step or the test-all search
+    Cubic cu;
+    if (disk_in || ang || test_all) cu = hermite_coef(h, ua, wa, ub, wb);
+    // ---- disk (only the radius is kept across the sphere search; the disk
+    // line is formed after it, so little stays live across that call)
+    bool disk_hit = false;
+    double r_ev;
+    const double sigma = sm.sigma[t];
+    if (disk_in) {
+        const double tt = (next_disk - pa) / h;
+        const double u_ev = hermite_eval(cu, tt);
+        if (u_ev > 0.0) {
+            r_ev = 1.0 / u_ev;
+            disk_hit = r_ev >= p.disk_r_in && r_ev <= p.disk_r_out;
+        }
     }
     if (ang) {
         // Conservative radial extent of the step's polyline. Its vertices lie
@@ -384,21 +405,17 @@ __device__ BHRT_INL_EVT bool step_events(const KParams& p, SM& sm, int t, double
         sm.next_disk[t] = next_disk;
         sm.sigma[t] = sg;
     }
-    float next_sph = sm.next_sph[t];
     if (!test_all && sph_here) {
-        next_sph = CUDART_INF_F;
         const float fb = (float)pb;
-        for (int i = 0; i < nc; ++i) {
+        for (unsigned m = pass; m; m &= m - 1) {
+            const int i = __ffs(m) - 1;
             float lo = sm.lo[i][t], hi = sm.hi[i][t];
-            if (hi < fb) {
-                while (hi < fb) {
-                    lo += 2.0f * (float)PI_D;
-                    hi += 2.0f * (float)PI_D;
-                }
-                sm.lo[i][t] = lo;
-                sm.hi[i][t] = hi;
+            while (hi < fb) {
+                lo += 2.0f * (float)PI_D;
+                hi += 2.0f * (float)PI_D;
             }
-            next_sph = fminf(next_sph, lo);
+            sm.lo[i][t] = lo;
+            sm.hi[i][t] = hi;
         }
         sm.next_sph[t] = next_sph;
     }
