@@ -4,6 +4,7 @@
 // reference's own operation order, so the device sees bit-identical values.
 #pragma once
 
+#include <cstddef>
 #include <cstdint>
 
 #include "bhrt_cuda.h"
@@ -19,6 +20,9 @@ struct alignas(16) CullList {
     uint8_t k[kCullSlots];      // sphere indices, increasing
     float win[kCullSlots][4];   // (lo, hi) unwrapped window angle, (rlo, rhi) radial extent
 };
+// the scene kernel reads (n, next_lo, k) as one int4 and the windows as float4s
+static_assert(offsetof(CullList, k) == 8 && offsetof(CullList, win) == 16 && sizeof(CullList) == 144,
+              "CullList layout");
 
 // Render counters: kStatSlots copies of the 8 counter words, kStatStride
 // words apart (own 128-byte line each). Warps add their steps / rejections /

@@ -126,19 +126,24 @@ __device__ BHRT_INL_SETUP double events_setup(const KParams& p, SM& sm, int t, V
         int bin = (int)(th * (float)(p.cull_bins / PI_D));
         bin = bin < 0 ? 0 : (bin >= p.cull_bins ? p.cull_bins - 1 : bin);
         const CullList* L = static_cast<const CullList*>(p.cull) + (2 * bin + (flip ? 1 : 0));
-        const int2 hdr = __ldg(reinterpret_cast<const int2*>(L));
-        nc = hdr.x;
+        // header (n, next_lo, k[0..7]) and the first windows in one round of
+        // loads: most lists are short, so the ray waits one memory latency
+        const int4 hd = __ldg(reinterpret_cast<const int4*>(L));
+        const float4* W = reinterpret_cast<const float4*>(L->win);
+        const float4 w0 = __ldg(W), w1 = __ldg(W + 1), w2 = __ldg(W + 2);
+        nc = hd.x;
         if (nc > 0) {
-            next_sph = __int_as_float(hdr.y);
-            const uint2 kk = __ldg(reinterpret_cast<const uint2*>(L->k));
-            const float4* W = reinterpret_cast<const float4*>(L->win);
-            for (int i = 0; i < nc; ++i) {
-                const float4 w = __ldg(W + i);
-                sm.lo[i][t] = w.x;
-                sm.hi[i][t] = w.y;
-                sm.rlo[i][t] = w.z;
-                sm.rhi[i][t] = w.w;
-                sm.k[i][t] = (unsigned char)((i < 4 ? kk.x : kk.y) >> (8 * (i & 3)));
+            next_sph = __int_as_float(hd.y);
+#pragma unroll
+            for (int i = 0; i < kSlots; ++i) {
+                if (i < nc) {
+                    const float4 w = i == 0 ? w0 : (i == 1 ? w1 : (i == 2 ? w2 : __ldg(W + i)));
+                    sm.lo[i][t] = w.x;
+                    sm.hi[i][t] = w.y;
+                    sm.rlo[i][t] = w.z;
+                    sm.rhi[i][t] = w.w;
+                    sm.k[i][t] = (unsigned char)((unsigned)(i < 4 ? hd.z : hd.w) >> (8 * (i & 3)));
+                }
             }
         }
     } else if (ns > 0) {
