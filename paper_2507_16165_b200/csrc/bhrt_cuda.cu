@@ -22,7 +22,7 @@ namespace bhrt_b200 {
 
 int launch_trace(const KParams& p, cudaStream_t st, int* launches, cudaEvent_t* ev);
 void launch_table_build(const KParams& p, double* smp, double* ends, int32_t* kind, int32_t* n, cudaStream_t st);
-void launch_table_bind(const KParams& p, double* ends, double* psi0, double u0, cudaStream_t st);
+void launch_table_bind(const KParams& p, double* ends, double* meta, double u0, cudaStream_t st);
 void launch_trace_polylines(const KParams& p, const double* rays, long long n, bhrt_ray_record* records,
                             double* pts, int cap, int* npoly, cudaStream_t st);
 void launch_trace_rays(const KParams& p, const double* rays, long long n, bhrt_ray_record* records,
@@ -191,7 +191,7 @@ struct bhrt_ctx {
     DevBuf<uint8_t> out;
     DevBuf<unsigned long long> stats;
     DevBuf<CullList> cull;  // KParams::cull, 2 * kCullBins lists
-    DevBuf<double> tab_smp, tab_ends, tab_psi0;
+    DevBuf<double> tab_smp, tab_ends, tab_meta;
     DevBuf<int32_t> tab_kind, tab_n;
     bool has_table = false;
     double table_key[10] = {0};
@@ -442,7 +442,7 @@ void bhrt_ctx_destroy(bhrt_ctx* c) {
     if (c->host_out) cudaFreeHost(c->host_out);
     c->tab_smp.release();
     c->tab_ends.release();
-    c->tab_psi0.release();
+    c->tab_meta.release();
     c->tab_kind.release();
     c->tab_n.release();
     delete c;
@@ -591,7 +591,7 @@ int bhrt_ctx_set_scene(bhrt_ctx* c, const bhrt_scene* s, bhrt_status_info* info)
         const size_t E = static_cast<size_t>(s->table_entries);
         if (!c->has_table || std::memcmp(key, c->table_key, sizeof key) != 0) {
             if (c->tab_smp.ensure(E * s->table_samples * 2) || c->tab_ends.ensure(E * 4) ||
-                c->tab_kind.ensure(E) || c->tab_n.ensure(E) || c->tab_psi0.ensure(E))
+                c->tab_kind.ensure(E) || c->tab_n.ensure(E) || c->tab_meta.ensure(4 * E))
                 return set_info(info, BHRT_DEVICE, -1, -1, "table alloc failed");
             launch_table_build(k, c->tab_smp.p, c->tab_ends.p, c->tab_kind.p, c->tab_n.p, c->up_stream);
             CK(cudaGetLastError());
@@ -603,10 +603,10 @@ int bhrt_ctx_set_scene(bhrt_ctx* c, const bhrt_scene* s, bhrt_status_info* info)
         k.tab_ends = c->tab_ends.p;
         k.tab_kind = c->tab_kind.p;
         k.tab_n = c->tab_n.p;
-        k.tab_psi0 = c->tab_psi0.p;
+        k.tab_meta = c->tab_meta.p;
         // bind the frame: each entry's inbound psi of the camera's u0 (oracle prep_table)
         const double u0 = 1.0 / hnorm(hsub(hv(s->cam_pos), hv(s->center)));
-        launch_table_bind(k, c->tab_ends.p, c->tab_psi0.p, u0, c->up_stream);
+        launch_table_bind(k, c->tab_ends.p, c->tab_meta.p, u0, c->up_stream);
         CK(cudaGetLastError());
     }
     k.grow = c->tables.p;

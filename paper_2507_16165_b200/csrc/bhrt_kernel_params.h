@@ -122,7 +122,7 @@ struct KParams {
     const double* tab_ends;
     const int32_t* tab_kind;
     const int32_t* tab_n;
-    const double* tab_psi0;
+    const double* tab_meta;  // per frame, 4 doubles per entry: psi0, psi_end, psi_esc, kind | n << 32
     int32_t table_entries, table_ns;
     double table_b_max, table_dpsi;
     double inv_table_b_max, inv_table_dpsi;  // RN(1/.) from the host (exact quotients: table.cu div_by)

@@ -102,10 +102,13 @@ struct TabEntry {
     double pend, pesc, psi0;  // ends[0], ends[3], the camera's inbound psi
 };
 
-__device__ __forceinline__ TabEntry tab_entry(const TabView& T, const double* psi0, int e) {
-    const double2 e01 = __ldg(reinterpret_cast<const double2*>(T.ends + 4 * (size_t)e));
-    const double2 e23 = __ldg(reinterpret_cast<const double2*>(T.ends + 4 * (size_t)e + 2));
-    return {__ldg(&T.kind[e]), __ldg(&T.n[e]), e01.x, e23.y, __ldg(&psi0[e])};
+// The frame's packed entry record (bind_table_kernel): (psi0, psi_end),
+// (psi_esc, kind | n << 32) — two 16-byte loads per entry.
+__device__ __forceinline__ TabEntry tab_entry(const double* meta, int e) {
+    const double2 a = __ldg(reinterpret_cast<const double2*>(meta + 4 * (size_t)e));
+    const double2 b = __ldg(reinterpret_cast<const double2*>(meta + 4 * (size_t)e + 2));
+    const long long kn = __double_as_longlong(b.y);
+    return {(int)(kn & 0xffffffff), (int)(kn >> 32), a.y, b.x, a.x};
 }
 
 // oracle table_u: u on entry e at orbit angle psi (mirrored past periapsis).
@@ -225,13 +228,21 @@ __global__ void __launch_bounds__(128) build_table_kernel(const __grid_constant_
 }
 
 // psi_esc per entry (needs the finished entry) and, per frame, psi0 of u0.
-__global__ void bind_table_kernel(const __grid_constant__ KParams p, double* ends, double* psi0,
+__global__ void bind_table_kernel(const __grid_constant__ KParams p, double* ends, double* meta,
                                   double u0, int with_esc) {
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= p.table_entries) return;
     TabView T{p.tab_smp, ends, p.tab_kind, p.tab_n, p.table_ns, p.table_dpsi, 1.0 / p.table_dpsi};
     if (with_esc) ends[4 * (size_t)e + 3] = inbound_psi(T, e, p.u_esc);
-    if (psi0) psi0[e] = inbound_psi(T, e, u0);
+    if (meta) {  // the frame's packed record (tab_entry)
+        const double* E = ends + 4 * (size_t)e;
+        const long long kn = (long long)(uint32_t)T.kind[e] | ((long long)T.n[e] << 32);
+        double* m = meta + 4 * (size_t)e;
+        m[0] = inbound_psi(T, e, u0);
+        m[1] = E[0];
+        m[2] = E[3];
+        m[3] = __longlong_as_double(kn);
+    }
 }
 
 // oracle table_plan
@@ -331,7 +342,7 @@ __global__ void __launch_bounds__(128, BHRT_TAB_MINB) trace_table_kernel(const _
                 int ie = (int)floor(x);
                 if (ie > N - 2) ie = N - 2;
                 BHRT_ASSERT(ie >= 0 && ie + 1 < N);
-                const TabEntry Mi = tab_entry(T, p.tab_psi0, ie), Mj = tab_entry(T, p.tab_psi0, ie + 1);
+                const TabEntry Mi = tab_entry(p.tab_meta, ie), Mj = tab_entry(p.tab_meta, ie + 1);
                 double f = x - (double)ie;
                 if (Mi.kind == 3) f = 1.0;
                 const double p0i = Mi.psi0, p0j = Mj.psi0;
@@ -430,8 +441,8 @@ void launch_table_build(const KParams& p, double* smp, double* ends, int32_t* ki
     bind_table_kernel<<<(p.table_entries + 255) / 256, 256, 0, st>>>(q, ends, nullptr, 0.0, 1);
 }
 
-void launch_table_bind(const KParams& p, double* ends, double* psi0, double u0, cudaStream_t st) {
-    bind_table_kernel<<<(p.table_entries + 255) / 256, 256, 0, st>>>(p, ends, psi0, u0, 0);
+void launch_table_bind(const KParams& p, double* ends, double* meta, double u0, cudaStream_t st) {
+    bind_table_kernel<<<(p.table_entries + 255) / 256, 256, 0, st>>>(p, ends, meta, u0, 0);
 }
 
 void launch_table_trace(const KParams& p, cudaStream_t st) {
