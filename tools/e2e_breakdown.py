@@ -26,7 +26,7 @@ def main():
     fr.render(sb)
     print("set_scene          min %.3f  mean %.3f ms" % timed(lambda: fr.set_scene(sb)))
     print("render_device+fin  min %.3f  mean %.3f ms" % timed(lambda: (fr.render_device(), fr.finish())))
-    for b in (1, 2, 4, 8, 16):
+    for b in (1, 8, 16, 24, 32, 48, 64):
         print(f"render bands={b:2d}   min %.3f  mean %.3f ms" % timed(lambda: fr.render(sb, bands=b)))
     out = fr.out.view(-1)
     host = fr.host.view(-1)
