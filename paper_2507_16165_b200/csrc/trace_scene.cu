@@ -46,9 +46,7 @@ struct SceneSmT {
     static constexpr int kNS = NS;
     double e2[3][NS], n[3][NS];  // e1 is the per-frame KParams::cam_e1
     double sigma[NS], energy[NS], next_disk[NS];
-    float lo[kSlots][NS], hi[kSlots][NS];   // angular window (unwrapped phi)
-    float rlo[kSlots][NS], rhi[kSlots][NS]; // radial extent of the circle
-    unsigned char k[kSlots][NS];
+    int list[NS];  // the ray's candidate list (KParams::cull record), read in place
     int nc[NS];
     float next_sph[NS];
 };
@@ -86,6 +84,31 @@ __device__ __forceinline__ float atan2_cull(float y, float x) {
     return copysignf(r, y);
 }
 
+// A candidate window recurs every 2 pi of orbit angle (the circle is the
+// same each winding). The occurrence in use at angle f is the first whose
+// end is not before f; the lists keep the first occurrence and every ray
+// derives its current one (fp32, k * 2 pi by one fma: within 1e-5 rad of
+// repeated additions, far inside the windows' 1e-4 rad margins), so no
+// per-ray window state is stored.
+__device__ __forceinline__ float2 window_at(float4 w, float f) {
+    if (w.y >= f) return make_float2(w.x, w.y);
+    constexpr float k2pi = 2.0f * (float)PI_D;
+    float kf = ceilf((f - w.y) * (1.0f / k2pi));
+    float hi = fmaf(kf, k2pi, w.y);
+    while (hi < f) {
+        kf += 1.0f;
+        hi = fmaf(kf, k2pi, w.y);
+    }
+    return make_float2(fmaf(kf, k2pi, w.x), hi);
+}
+
+__device__ __forceinline__ const CullList& cull_list(const KParams& p, int li) {
+    return static_cast<const CullList*>(p.cull)[li];
+}
+__device__ __forceinline__ int cull_k(const CullList& L, int i) {
+    return __ldg(reinterpret_cast<const unsigned char*>(L.k) + i);
+}
+
 // Disk line + sphere candidates (oracle ray_events_setup). Returns the first
 // event angle.
 template <class SM>
@@ -117,7 +140,7 @@ __device__ BHRT_INL_SETUP double events_setup(const KParams& p, SM& sm, int t, V
     if (p.cull && ns > 0) {
         // plane-angle bin and orientation -> the frame's precomputed list of
         // conservative candidates with their windows (KParams::cull,
-        // build_cull_lists_kernel): a 144-byte record copied to the ray's slots
+        // build_cull_lists_kernel), read in place
         const float na = (float)(n.x * p.cull_a[0] + n.y * p.cull_a[1] + n.z * p.cull_a[2]);
         const float nb = (float)(n.x * p.cull_b[0] + n.y * p.cull_b[1] + n.z * p.cull_b[2]);
         float th = atan2_cull(nb, na);  // lists cover +-1e-5 rad beyond their bin
@@ -125,27 +148,12 @@ __device__ BHRT_INL_SETUP double events_setup(const KParams& p, SM& sm, int t, V
         if (flip) th += (float)PI_D;
         int bin = (int)(th * (float)(p.cull_bins / PI_D));
         bin = bin < 0 ? 0 : (bin >= p.cull_bins ? p.cull_bins - 1 : bin);
-        const CullList* L = static_cast<const CullList*>(p.cull) + (2 * bin + (flip ? 1 : 0));
-        // header (n, next_lo, k[0..7]) and the first windows in one round of
-        // loads: most lists are short, so the ray waits one memory latency
-        const int4 hd = __ldg(reinterpret_cast<const int4*>(L));
-        const float4* W = reinterpret_cast<const float4*>(L->win);
-        const float4 w0 = __ldg(W), w1 = __ldg(W + 1), w2 = __ldg(W + 2);
+        const int li = 2 * bin + (flip ? 1 : 0);
+        // the ray reads its list's windows in place at event steps (window_at)
+        const int2 hd = __ldg(reinterpret_cast<const int2*>(&cull_list(p, li)));
         nc = hd.x;
-        if (nc > 0) {
-            next_sph = __int_as_float(hd.y);
-#pragma unroll
-            for (int i = 0; i < kSlots; ++i) {
-                if (i < nc) {
-                    const float4 w = i == 0 ? w0 : (i == 1 ? w1 : (i == 2 ? w2 : __ldg(W + i)));
-                    sm.lo[i][t] = w.x;
-                    sm.hi[i][t] = w.y;
-                    sm.rlo[i][t] = w.z;
-                    sm.rhi[i][t] = w.w;
-                    sm.k[i][t] = (unsigned char)((unsigned)(i < 4 ? hd.z : hd.w) >> (8 * (i & 3)));
-                }
-            }
-        }
+        if (nc > 0) next_sph = __int_as_float(hd.y);
+        sm.list[t] = li;
     } else if (ns > 0) {
         nc = -1;  // no culling basis (never for a valid camera): every event step tests every sphere
     }
@@ -220,12 +228,15 @@ __device__ BHRT_INL_SPH bool sphere_search(const KParams& p, const SM& sm, int t
             k = a;
         } else {
             if (!(act & (1u << a))) continue;
-            k = sm.k[a][t];
+            const CullList& L = cull_list(p, sm.list[t]);
+            k = cull_k(L, a);
             BHRT_ASSERT(k < p.n_spheres);
+            // the window occurrence step_events tested (at the step start)
+            const float2 wn = window_at(__ldg(reinterpret_cast<const float4*>(L.win[a])), fpa);
             // clamp in float first: windows may be infinite
             const float fS = (float)S;
-            j0 = (int)fminf(fmaxf(floorf((sm.lo[a][t] - fpa) * rdl) - 1.0f, 0.0f), fS);
-            j1 = (int)fminf(fmaxf(floorf((sm.hi[a][t] - fpa) * rdl) + 1.0f, 0.0f), fS - 1.0f);
+            j0 = (int)fminf(fmaxf(floorf((wn.x - fpa) * rdl) - 1.0f, 0.0f), fS);
+            j1 = (int)fminf(fmaxf(floorf((wn.y - fpa) * rdl) + 1.0f, 0.0f), fS - 1.0f);
         }
         j1 = min(j1, best_j);
         if (j0 > j1) continue;
@@ -302,27 +313,21 @@ __device__ BHRT_INL_EVT bool step_events(const KParams& p, SM& sm, int t, double
     // so the sphere half is skipped entirely — disk-only event steps.
     const bool sph_here = test_all || sm.next_sph[t] <= (float)pb;
     unsigned act = 0;
-    unsigned ang = 0;   // candidates whose angular window meets the step
-    unsigned pass = 0;  // candidates whose window ends inside the step (moved on below)
+    unsigned ang = 0;  // candidates whose angular window meets the step
     float next_sph = sm.next_sph[t];
+    const CullList* L = nullptr;
     if (!test_all && sph_here) {
-        // one pass over the slots: the angular test, and the next window
-        // start after this step (a window ending before pb moves on by 2 pi,
-        // stored after the search, which reads the windows as they are)
+        // one pass over the list: the occurrence of each window in use at
+        // the step start meets the step or not; the next window start after
+        // the step is the first occurrence not ending before pb
+        L = &cull_list(p, sm.list[t]);
         const float fa = (float)pa, fb = (float)pb;
         next_sph = CUDART_INF_F;
         for (int i = 0; i < nc; ++i) {
-            float lo = sm.lo[i][t];
-            float hi = sm.hi[i][t];
-            if (lo <= fb && hi >= fa) ang |= 1u << i;
-            if (hi < fb) {
-                pass |= 1u << i;
-                while (hi < fb) {
-                    lo += 2.0f * (float)PI_D;
-                    hi += 2.0f * (float)PI_D;
-                }
-            }
-            next_sph = fminf(next_sph, lo);
+            const float4 w = __ldg(reinterpret_cast<const float4*>(L->win[i]));
+            const float2 wa_ = window_at(w, fa);
+            if (wa_.x <= fb && wa_.y >= fa) ang |= 1u << i;
+            next_sph = fminf(next_sph, wa_.y >= fb ? wa_.x : window_at(w, fb).x);
         }
     }
     // the step's Hermite interpolant, needed for a disk crossing, a window
@@ -363,7 +368,8 @@ __device__ BHRT_INL_EVT bool step_events(const KParams& p, SM& sm, int t, double
         }
         for (unsigned m = ang; m; m &= m - 1) {
             const int i = __ffs(m) - 1;
-            if (sm.rlo[i][t] <= shi && sm.rhi[i][t] >= slo) act |= 1u << i;
+            const float2 r = __ldg(reinterpret_cast<const float2*>(L->win[i]) + 1);  // (rlo, rhi)
+            if (r.x <= shi && r.y >= slo) act |= 1u << i;
         }
     }
     bool sph_hit = false;
@@ -410,20 +416,7 @@ __device__ BHRT_INL_EVT bool step_events(const KParams& p, SM& sm, int t, double
         sm.next_disk[t] = next_disk;
         sm.sigma[t] = sg;
     }
-    if (!test_all && sph_here) {
-        const float fb = (float)pb;
-        for (unsigned m = pass; m; m &= m - 1) {
-            const int i = __ffs(m) - 1;
-            float lo = sm.lo[i][t], hi = sm.hi[i][t];
-            while (hi < fb) {
-                lo += 2.0f * (float)PI_D;
-                hi += 2.0f * (float)PI_D;
-            }
-            sm.lo[i][t] = lo;
-            sm.hi[i][t] = hi;
-        }
-        sm.next_sph[t] = next_sph;
-    }
+    if (!test_all && sph_here) sm.next_sph[t] = next_sph;
     next_ev = dmin(next_disk, (double)next_sph);
     return disk_hit || sph_hit;
 }
