@@ -88,3 +88,29 @@ def test_ragged_sizes(wh):
     sb = scenes.config(2, *wh)
     res = compare(sb)
     assert res["steps_equal"]
+
+
+def test_sphere_hits_after_a_full_winding():
+    """Rays with impact parameter just above the critical one wind around
+    the hole before escaping; small spheres hugging the photon sphere are
+    then hit on a later winding, where the kernel tests a candidate window's
+    k-th occurrence (window_at: the list keeps the first, rays derive the one
+    in use). Same objects and hit points as the oracle, and some hits come
+    after more than one full turn."""
+    sb = scenes.config(2, 96, 96)
+    sb.set(disk_enabled=0, cam_pos=scenes.inclined_camera(12.0, 60.0), vertical_fov=0.9)
+    rng = np.random.default_rng(5)
+    sph = []
+    for _ in range(40):
+        d = rng.normal(size=3)
+        d /= np.linalg.norm(d)
+        sph.append(sphere(tuple(d * rng.uniform(3.4, 4.2)), float(rng.uniform(0.15, 0.35)),
+                          tuple(rng.random(3))))
+    sb.set_spheres(sph)
+    res = compare(sb)
+    assert res["steps_equal"]
+    from paper_2507_16165_b200 import render
+    from paper_2507_16165_b200.abi import OBJ_SPHERE
+    _, rec = render.render_rows(sb, 0, sb.s.height, 1, records=True)
+    late = (rec["object"] == OBJ_SPHERE) & (rec["phi"] > 2.0 * np.pi)
+    assert late.sum() > 0, "no sphere hit after a full winding"
