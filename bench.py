@@ -230,12 +230,12 @@ def measure_secondary(device: int, peak: float, reps: int = 3, rank: int = 0, wo
         ctx.render_async(buf.data_ptr(), stream=st.cuda_stream)
         ctx.finish()
     scs = [scenes.config(4, frame=f) for f in range(frames)]
-    # three contexts on three streams in turn: frame f+1's scene upload (cull
-    # table on the host, async copies) proceeds while frame f renders, and
-    # frame f+1's kernel fills the SMs while frame f's longest blocks drain
-    # (1/2/3 streams: 426/460/472 frames/s, tools/orbit_time.py); each
-    # finish() waits for its own frame only
-    NC = 3
+    # six contexts on six streams in turn: frame f+1's scene upload (cull
+    # lists built on the device, async copies) proceeds while frame f
+    # renders, and later frames' kernels fill the SMs while the close-camera
+    # frames' longest rays drain (3/4/6/8 streams: 533/548/556/559 frames/s,
+    # tools/orbit_time.py); each finish() waits for its own frame only
+    NC = 6
     ctxs = [ctx] + [render.Context(device) for _ in range(NC - 1)]
     bufs = [buf] + [torch.empty_like(buf) for _ in range(NC - 1)]
     strs = [st] + [torch.cuda.Stream(device) for _ in range(NC - 1)]

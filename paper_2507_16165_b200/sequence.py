@@ -44,9 +44,10 @@ class SequenceRenderer:
     writer thread (PPM files, or a callback)."""
 
     # frames in flight on the device: each has its own context (scene),
-    # device image and stream, so frame f+1's kernel fills the SMs while
-    # frame f's longest blocks drain (config 4: 426 -> 460 frames/s for 2)
-    NF = 2
+    # device image and stream, so later frames' kernels fill the SMs while a
+    # frame's longest rays drain (config 4 with PPM files, 3 writers:
+    # 2 / 3 / 4 in flight -> 493 / 515 / 531 frames/s)
+    NF = 4
 
     def __init__(self, device: int = 0, writers: int = 3):
         import torch
@@ -66,10 +67,12 @@ class SequenceRenderer:
         t = self.torch
         self.dev = [t.empty((h, w, 3), dtype=t.uint8, device=f"cuda:{self.device}")
                     for _ in range(self.NF)]
-        # pinned buffers: one per writer thread, one queued, one receiving the
-        # next frame; a buffer is reused only after its writer returned it
+        # pinned buffers: one per frame in flight (rendered, not yet handed
+        # over), one queued, one per writer thread — the most that can be
+        # held at once, so taking a free one never waits on the loop itself;
+        # a buffer is reused only after its writer returned it
         self.host = [t.empty((h, w, 3), dtype=t.uint8, pin_memory=True)
-                     for _ in range(self.writers + 2)]
+                     for _ in range(self.NF + 1 + self.writers)]
         self.free: queue.Queue = queue.Queue()
         for b in self.host:
             self.free.put(b)

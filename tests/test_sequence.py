@@ -39,3 +39,28 @@ def test_sequence_renderer_writes_every_frame(tmp_path):
     for sb, p in zip(scs, paths):
         want = render.render_rows(sb, 0, sb.s.height).reshape(sb.s.height, sb.s.width, 3)
         assert open(p, "rb").read() == save_ppm_bytes(want)
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("nf,writers", [(6, 1), (2, 1), (4, 3)])
+def test_sequence_renderer_any_depth_never_starves(tmp_path, nf, writers):
+    """Frames in flight beyond the writer count: the pinned pool holds one
+    buffer per frame in flight, one queued and one per writer, so the render
+    loop never waits on a buffer only it could release (a pool of writers + 2
+    deadlocked for 6 in flight)."""
+    from paper_2507_16165_b200 import render, scenes
+    from paper_2507_16165_b200.sequence import SequenceRenderer
+
+    class Deep(SequenceRenderer):
+        NF = nf
+
+    scs = [scenes.config(4, 64, 36, frame=f) for f in range(0, 120, 9)]
+    paths = [os.path.join(tmp_path, f"f{i}.ppm") for i in range(len(scs))]
+    r = Deep(0, writers=writers)
+    res = r.render(scs, paths)
+    r.close()
+    assert res["frames"] == len(scs)
+    for sb, p in zip(scs, paths):
+        want = render.render_rows(sb, 0, sb.s.height).reshape(sb.s.height, sb.s.width, 3)
+        assert open(p, "rb").read() == save_ppm_bytes(want)

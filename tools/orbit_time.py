@@ -58,5 +58,5 @@ for sb in scs:
     tot += e0.elapsed_time(e1)
 ctx.close()
 print(f"kernel-only sum: {tot / frames:.3f} ms/frame ({frames * 1e3 / tot:.1f} frames/s)")
-for nctx, nst in ((2, 1), (2, 2), (3, 3), (4, 2)):
+for nctx, nst in ((3, 3), (4, 4), (6, 6), (8, 8)):
     run(nctx, nst)
