@@ -370,7 +370,8 @@ __device__ static __noinline__ void sample_direction(const KParams& p, V3 d, dou
 #ifndef BHRT_INL_SETUP
 #define BHRT_INL_SETUP  // compiler's choice (single call site)
 #endif
-__device__ static BHRT_INL_SHADE void shade_sample(const KParams& p, int obj, int sphere, V3 pt, double rgb[3]) {
+__device__ static __forceinline__ void shade_sample_body(const KParams& p, int obj, int sphere, V3 pt,
+                                                         double rgb[3]) {
     rgb[0] = rgb[1] = rgb[2] = 0.0;
     if (obj == BHRT_OBJ_SKY) {
         if (p.sky_kind == BHRT_SKY_CHECKER) {
@@ -446,6 +447,12 @@ __device__ static BHRT_INL_SHADE void shade_sample(const KParams& p, int obj, in
     }
 }
 
+// Per translation unit: inlined (default) or a call (BHRT_INL_SHADE), see
+// finish_sample's INL_SHADE for the per-instantiation choice.
+__device__ static BHRT_INL_SHADE void shade_sample(const KParams& p, int obj, int sphere, V3 pt, double rgb[3]) {
+    shade_sample_body(p, obj, sphere, pt, rgb);
+}
+
 // render.cpp:42-48: inv = 1/spp, round-half-away-from-zero, clamp to [0,255].
 __device__ __forceinline__ void store_pixel(uint8_t* o, const double acc[3], double inv) {
     // inv = 1.0 / spp, formed once on the host (KParams::inv_spp)
@@ -460,6 +467,7 @@ __device__ __forceinline__ void store_pixel(uint8_t* o, const double acc[3], dou
 // optional record, and in fused mode the sample colour, the pixel sum in
 // sample order over the spp adjacent lanes (render.cpp:25-32) and the 8-bit
 // store. A failed sample fails its pixel (lowest failing pixel -> stats[3]).
+template <bool INL_SHADE = false>
 __device__ __forceinline__ void finish_sample(const KParams& p, bool valid, const SampleId& id, int obj,
                                               int sphere, V3 point, double phi, unsigned steps,
                                               unsigned rej) {
@@ -489,7 +497,12 @@ __device__ __forceinline__ void finish_sample(const KParams& p, bool valid, cons
 #ifdef BHRT_EXPERIMENT_NOSHADE
             rgb[0] = point.x;  // timing experiment only: no shading code
 #else
-            shade_sample(p, obj, sphere, point, rgb);
+        {
+            if (INL_SHADE)
+                shade_sample_body(p, obj, sphere, point, rgb);
+            else
+                shade_sample(p, obj, sphere, point, rgb);
+        }
 #endif
     }
     const int lane = threadIdx.x & 31;

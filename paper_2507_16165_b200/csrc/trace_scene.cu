@@ -7,9 +7,10 @@
 // event steps and escape touch. Operation order mirrors the oracle
 // (oracle/bhrt_oracle.c trace_scene / step_events / escape_dir), so records
 // are bit-identical up to libdevice transcendentals outside the step.
-// The shading is called out of line in this kernel: it keeps its code out
-// of the step loop's instruction stream (config 2: 7.72 -> 7.64 ms); the
-// table kernel keeps it inline (config 3: 2.32 vs 2.36 ms out of line).
+// The shading and the escape direction are inlined in the RKF45
+// instantiation (config 2: 5.79 -> 5.71 ms late in round 2; out of line won
+// earlier, 7.72 -> 7.64, when the kernel held more state) and called out of
+// line in the RK4 one (config 0: 1.20 vs 1.26 ms); the table kernel inlines.
 #ifndef BHRT_INL_SHADE
 #define BHRT_INL_SHADE __noinline__
 #endif
@@ -431,7 +432,7 @@ __device__ __forceinline__ V3 tangent_dir(V3 e1, V3 e2, double phi, double u, do
 // Oracle escape_dir(): tangent at the r = escape_radius crossing of the last
 // step (Hermite + 2 Newton iterations, u' from the first integral).
 template <class SM>
-__device__ BHRT_INL_ESC V3 escape_dir(const KParams& p, SM& sm, int t, bool has_step, double pa,
+__device__ __forceinline__ V3 escape_dir_body(const KParams& p, SM& sm, int t, bool has_step, double pa,
                                       double ua, double wa, double pb, double ub, double wb) {
     const V3 e1 = vld(p.cam_e1), e2 = ld3(sm.e2, t);
 #ifdef BHRT_EXPERIMENT_NOESC
@@ -453,6 +454,14 @@ __device__ BHRT_INL_ESC V3 escape_dir(const KParams& p, SM& sm, int t, bool has_
     const double q = sm.energy[t] - us * us + M2 * us * us * us;
     const double ws = -sqrt(q > 0.0 ? q : 0.0);
     return tangent_dir(e1, e2, pa + h * tt, us, ws);
+}
+// The RK4 instantiation calls it out of line (its registers stay off the
+// step loop: config 0 1.20 vs 1.26 ms inlined); the RKF45 one inlines it
+// with the shading (config 2 5.79 -> 5.71 ms).
+template <class SM>
+__device__ BHRT_INL_ESC V3 escape_dir(const KParams& p, SM& sm, int t, bool has_step, double pa,
+                                      double ua, double wa, double pb, double ub, double wb) {
+    return escape_dir_body(p, sm, t, has_step, pa, ua, wa, pb, ub, wb);
 }
 
 // Straight radial ray (geodesic.cpp:175-187) with scene hit tests.
@@ -598,7 +607,7 @@ __global__ void __launch_bounds__(kBlock, INTEG == BHRT_INTEGRATOR_RK4 ? BHRT_SC
                     H.obj = BHRT_OBJ_HORIZON;
                 } else if (u <= p.u_esc && w < 0.0) {
                     H.obj = BHRT_OBJ_SKY;
-                    H.point = escape_dir(p, sm, t, false, 0.0, 0.0, 0.0, phi, u, w);
+                    H.point = escape_dir_body(p, sm, t, false, 0.0, 0.0, 0.0, phi, u, w);
                 } else {
                     // One combined test per accepted step covers the common
                     // case — no event, capture, escape, numerical failure,
@@ -650,7 +659,7 @@ __global__ void __launch_bounds__(kBlock, INTEG == BHRT_INTEGRATOR_RK4 ? BHRT_SC
                             }
                             if (un <= p.u_esc && wn < 0.0) {
                                 H.obj = BHRT_OBJ_SKY;
-                                H.point = escape_dir(p, sm, t, true, phi, u, w, pn, un, wn);
+                                H.point = escape_dir_body(p, sm, t, true, phi, u, w, pn, un, wn);
                                 phi = pn;
                                 break;
                             }
@@ -674,7 +683,7 @@ __global__ void __launch_bounds__(kBlock, INTEG == BHRT_INTEGRATOR_RK4 ? BHRT_SC
                 H.point = escape_dir(p, sm, t, has_step, pp, up, wp, phi, u, w);
         }
     }
-    finish_sample(p, valid, id, H.obj, H.sphere, H.point, phi, nsteps, nrej);
+    finish_sample<INTEG == BHRT_INTEGRATOR_RKF45>(p, valid, id, H.obj, H.sphere, H.point, phi, nsteps, nrej);
     warp_add_stats(p.stats, nsteps, nrej, valid ? 1u : 0u);
 }
 
