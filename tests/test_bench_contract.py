@@ -105,3 +105,10 @@ def test_our_arm_line():
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] >= 3840 * 2160 * 3
     assert d["gpu_launches"] >= d["steps"]
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
+    # the drop-in C ABI e2e and the GPU through the reference's own harness
+    dr = d["e2e_dropin"]
+    assert dr["value"] > 0 and dr["image_equals_frame_renderer"]
+    hg = d.get("reference_harness_gpu")
+    if hg is not None:  # dropin/bhrt_bench_b200 built (needs /root/reference at build time)
+        assert "error" not in hg, hg
+        assert hg["value"] > 0 and len(hg["runs"]) == 5 and hg["seconds_per_run"] > 0
